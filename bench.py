@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark: binary forward pass on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload bcnn|bmlp|bgemm]
+                    [--batch B] [--impl ours|reference]
+
+One step = one forward pass of the workload over one batch of synthetic
+input per GPU (weak scaling: each rank owns its own batch slice; images
+are independent, so there is no collective on the data path — the only
+NCCL calls are the barrier and the max-over-ranks reduction of the
+timings).  Multi-GPU runs are launched with torchrun, one rank per GPU.
+
+`value`  — device throughput: inputs resident in HBM, K steps timed with
+           CUDA events on the launching stream (each step is one CUDA-graph
+           replay of the whole network), L2 flushed between steps.
+`e2e`    — the same metric through the public API `forward_batch` with host
+           uint8 images: pinned H2D copy + forward + D2H of the scores inside
+           the timed region.
+`roofline` — per-stage device times (CUDA events, eager launches on the
+           same stream), dominant stage's achieved bit-op/s against the
+           measured POPC-pipe peak of this B200.
+`cpu_baseline` — the CPU oracle port of the reference (oracle/, OpenMP
+           threads where the reference uses numba prange) on a bounded
+           sample, rank 0 only.
+`--impl reference` — the reference arm: that same CPU path timed on the
+           host for the same metric/config (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "images/sec (BMLP MNIST, BCNN CIFAR-10) at 1/2/4/8 B200; binary GEMM Gop/s"
+# Measured POPC pipe rate (tools/microbench/pipes.cu on this pool's B200:
+# 15.66 POPC/clk/SM -> 4.555e12 popc/s x 32 bit-MAC x 2 = 291.5 T bit-op/s).
+POPC_PEAK_TBITOPS = 4.555e12 * 64 / 1e12
+POPC_PEAK_SOURCE = "tools/microbench/pipes.cu popc_xor on B200 (profiles/pipes_r01.jsonl): 15.66 POPC/clk/SM"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- workloads
+
+def build_workload(name):
+    from paper_1705_07175_b200 import zoo
+    if name == "bcnn":
+        return zoo.bcnn_spec(), (32, 32, 3)
+    if name == "bmlp":
+        return zoo.bmlp_spec(), (784,)
+    raise ValueError(name)
+
+
+def cpu_sample(spec, shape, seconds: float, min_images: int, seed: int = 123):
+    """Time the CPU oracle (reference restatement) image by image, like the
+    reference's cli.py:101-104 loop, for about `seconds`."""
+    from oracle import oracle as o
+    net = o.OracleNetwork(spec)
+    rng = np.random.default_rng(seed)
+    imgs = rng.integers(0, 256, (max(min_images, 8),) + shape, dtype=np.uint8)
+    net.forward(imgs[0])  # warm caches
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        net.forward(imgs[n % imgs.shape[0]])
+        n += 1
+        dt = time.perf_counter() - t0
+        if n >= min_images and dt >= seconds:
+            break
+    return n / dt, n, dt, o.num_threads()
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return None
+    spec, shape = build_workload(args.workload)
+    per_step = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_sample(spec, shape, 0.0, per_step)
+    rates, total_n, total_t = [], 0, 0.0
+    threads = 0
+    for _ in range(args.steps):
+        r, n, dt, threads = cpu_sample(spec, shape, 0.0, per_step)
+        rates.append(r)
+        total_n += n
+        total_t += dt
+    value = total_n / total_t
+    return {
+        "metric": BASELINE_METRIC, "value": value, "unit": "images/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64-packed bits / int32 acc / f64 scores", "data": "synthetic",
+        "config": config_dict(args),
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} images per step, {args.steps} steps, per-image forward "
+                                   f"(oracle/oracle.c restatement of the reference packed kernels, OpenMP "
+                                   f"where the reference uses numba prange)"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def config_dict(args):
+    if args.workload == "bcnn":
+        wl = "BCNN VGG-style CIFAR-10 2x128C3-MP2-2x256C3-MP2-2x512C3-MP2-1024FC-1024FC-10, 32x32x3 u8"
+    else:
+        wl = "BinaryNet MLP 784-4096-4096-4096-10 on MNIST-shaped u8"
+    return {"workload": wl, "images_per_gpu_per_step": args.batch, "global_batch": args.batch * args.gpus,
+            "parallelism": f"dp{args.gpus} (batch slices, no collective)", "l2": "flushed between timed steps",
+            "weights": "seeded random +/-1 (paper_1705_07175_b200/zoo.py)"}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1705_07175_b200 import _lib, forward_batch, zoo
+    from paper_1705_07175_b200.network import Network
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    spec, shape = build_workload(args.workload)
+    B = args.batch
+    net = Network(spec, max_batch=B)
+    rng = np.random.default_rng(1000 + rank)
+    host_imgs = rng.integers(0, 256, (B, int(np.prod(shape))), dtype=np.uint8)
+    net.input_device.copy_(torch.from_numpy(host_imgs).to(dev))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also captures the CUDA graph for batch B)
+    for _ in range(max(args.warmup, 1)):
+        net.run(B)
+    barrier()
+
+    launches0 = _lib.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            net.run(B)
+            ev[i][1].record(stream)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    launches_direct = _lib.launch_count() - launches0
+    gpu_launches = net.launches_per_forward() * args.steps + launches_direct
+    value = args.steps * B * world / (total_ms / 1e3)
+
+    # e2e through the public API with host buffers (pinned H2D + D2H inside)
+    out = np.empty((B, net.classes), dtype=np.float64)
+    forward_batch(net, host_imgs, out)
+    barrier()
+    e2e_ev = []
+    for i in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.fill_(i & 0xFF)
+        a.record(stream)
+        forward_batch(net, host_imgs, out)
+        b.record(stream)
+        e2e_ev.append((a, b))
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    e2e_value = args.steps * B * world / (e2e_ms / 1e3)
+
+    # per-stage device time (eager launches on this stream, events)
+    stages = []
+    for st in net.stages:
+        reps = 5
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.launch(net, B, _dev_stream())
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            st.launch(net, B, _dev_stream())
+        b.record(stream)
+        torch.cuda.synchronize()
+        stages.append({"stage": st.name, "ms": a.elapsed_time(b) / reps, "bitops": 2 * stage_macs(st) * B})
+    stage_total = sum(s["ms"] for s in stages)
+    dom = max(stages, key=lambda s: s["ms"])
+    achieved = dom["bitops"] / (dom["ms"] / 1e3) / 1e12
+    result = {
+        "metric": BASELINE_METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64-packed bits / int32 acc / f64 scores", "data": "synthetic",
+        "config": config_dict(args) | {"global_batch": B * world},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": int(host_imgs.nbytes),
+                "d2h_bytes_per_step": int(out.nbytes)},
+        "gpu_launches": int(gpu_launches),
+        "bitops_per_image": 2 * zoo.macs_per_image(spec),
+        "achieved_tbitops_network": 2 * zoo.macs_per_image(spec) * value / world / 1e12,
+        "roofline": {"bound": "int-popc", "achieved": achieved, "peak": POPC_PEAK_TBITOPS, "unit": "Tbitop/s",
+                     "frac": achieved / POPC_PEAK_TBITOPS, "traffic": None, "kernel": dom["stage"],
+                     "kernel_share_of_step": dom["ms"] / stage_total, "peak_source": POPC_PEAK_SOURCE},
+        "stages": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in s.items()} for s in stages],
+    }
+    return result
+
+
+def _dev_stream():
+    from paper_1705_07175_b200 import _dev
+    return _dev.stream()
+
+
+def stage_macs(st) -> int:
+    """Algorithmic binary MACs per image of one device stage."""
+    from paper_1705_07175_b200 import network as nw
+    if isinstance(st, (nw._Input8Fused, nw._Input8Raw)):
+        return st.units * st.k * 8
+    if isinstance(st, (nw._DenseFused, nw._Dense)):
+        return st.rec.units * st.rec.input_len
+    if isinstance(st, (nw._ConvFused, nw._Conv, nw._ByteConvFused)):
+        return st.h_out * st.w_out * st.rec.filters * st.rec.k
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="bcnn", choices=["bcnn", "bmlp"])
+    ap.add_argument("--batch", type=int, default=None, help="images per GPU per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-sample", type=int, default=32)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.batch is None:
+        args.batch = 8192 if args.workload == "bcnn" else 16384
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    args.gpus = world if world > 1 else args.gpus
+
+    if args.impl == "reference":
+        res = run_reference_arm(args, rank)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu:
+            spec, shape = build_workload(args.workload)
+            rate, n, dt, threads = cpu_sample(spec, shape, args.cpu_seconds, 8)
+            res["cpu_baseline"] = {"value": rate, "unit": "images/s", "cores": threads, "kind": "port",
+                                   "sample": f"{n} images in {dt:.1f} s, per-image forward of the oracle port "
+                                             f"(oracle/oracle.c, OpenMP where the reference uses prange)"}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * bitnn_b200.h — C ABI of the B200-native binary forward pass.
+ *
+ * Drop-in boundary for the packed backend of the reference `bitnn`
+ * (/root/reference/pkg/src/bitnn).  Every entry point replaces one
+ * reference Numba kernel (`_kernels.py`) or one fused stage of the
+ * packed network (`network.py`), with the same data layout:
+ *
+ *   - packed lines are uint64 words, LSB-first, +1 -> bit 1, -1 -> bit 0,
+ *     each line padded to whole words with ZERO padding bits;
+ *   - every kernel writes its whole `out` (caller-provided, no
+ *     allocation inside), like the reference's caller-provided `out`
+ *     arrays (_kernels.py:15-16);
+ *   - a leading `batch` argument runs the same kernel over `batch`
+ *     independent images laid out back to back (the reference is
+ *     batch-1 only, network.py:506-522).
+ *
+ * All pointers are DEVICE pointers unless named `h_*`; `stream` is a
+ * cudaStream_t passed as void*.  Return value: 0 on success, otherwise a
+ * cudaError_t code (or B2_EINVAL for bad arguments); no entry point
+ * synchronizes the device.
+ *
+ * No torch types cross this boundary; the Python host layer
+ * (paper_1705_07175_b200/) binds it through ctypes.
+ */
+#ifndef BITNN_B200_H
+#define BITNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2_EINVAL 1000
+
+/* Threshold plan of one batchnorm+sign stage, already on the device.
+ * thresh:   int32 per channel, clamped to [-(B+1), B+1] where B bounds |acc|
+ *           (exact — see DESIGN.md "threshold clamping"); used by the fused
+ *           GEMM epilogues whose accumulators are int32;
+ * thresh64: the unclamped int64 thresholds (sentinels +-2^62), used by the
+ *           generic threshold-pack kernel (int64 / uint8 inputs);
+ * ge_dir:   uint8 per channel, 1 -> bit = acc >= t, 0 -> bit = acc <= t.
+ * Replaces BatchNormLayer.thresh/ge_dir (layers.py:146-191). */
+typedef struct b2_thresh {
+  const int32_t* thresh;
+  const int64_t* thresh64;
+  const uint8_t* ge_dir;
+} b2_thresh;
+
+/* ---------------------------------------------------------------- version */
+const char* b2_version(void);
+/* Number of kernel launches issued through this library since load
+ * (host-side counter, for the bench's gpu_launches claim). */
+int64_t b2_launch_count(void);
+
+/* ---------------------------------------------------------------- packing */
+
+/* _kernels.py:43-54 pack_lines: bit = !(x < 0) (0.0, -0.0, NaN -> 1).
+ * lines (n_lines, bits) float32 row-major -> out (n_lines, ceil(bits/64)). */
+int b2_pack_lines_f32(const float* lines, int64_t n_lines, int64_t bits, uint64_t* out, void* stream);
+
+/* _kernels.py:57-64 unpack_lines: -> +/-1.0 float32 (n_lines, bits). */
+int b2_unpack_lines_f32(const uint64_t* words, int64_t n_lines, int64_t bits, float* out, void* stream);
+
+/* _kernels.py:67-82 pack_byte_planes: uint8 (n_lines, bits) ->
+ * out (8, n_lines, ceil(bits/64)). */
+int b2_pack_byte_planes(const uint8_t* lines, int64_t n_lines, int64_t bits, uint64_t* out, void* stream);
+
+/* ---------------------------------------------------------------- GEMM */
+
+/* _kernels.py:85-106 bgemm_packed: out[m,n] = k - 2*popc(a_m XOR b_n), int32.
+ * a (m, wpl) row-packed, b (n, wpl) column-packed (both K-major), out (m, n). */
+int b2_bgemm(const uint64_t* a, int64_t m, const uint64_t* b, int64_t n, int64_t wpl, int32_t k, int32_t* out,
+             void* stream);
+
+/* _kernels.py:109-117 bgemv_packed, batched over `batch` activation lines:
+ * out[i, u] = k - 2*popc(w_u XOR x_i); w (units, wpl), x (batch, wpl). */
+int b2_bgemv(const uint64_t* w, int64_t units, int64_t wpl, const uint64_t* x, int64_t batch, int32_t k, int32_t* out,
+             void* stream);
+
+/* _kernels.py:120-147 count_plane_bits + bitplane_matvec, batched:
+ * planes (8, batch, wpl) as written by b2_pack_byte_planes -> out (batch,
+ * units) int64, w (units, wpl). */
+int b2_bitplane_gemv(const uint64_t* planes, int64_t batch, const uint64_t* w, int64_t units, int64_t wpl,
+                     int64_t* out, void* stream);
+
+/* ---------------------------------------------------------------- conv */
+
+/* _kernels.py:170-199 unroll_packed (bit im2col), batched: lines of `batch`
+ * images (channel axis iff c > 1, tensor.py:165-166) -> out
+ * (batch * h_out * w_out, ceil(kh*kw*c/64)); OOB window sites stay 0 bits. */
+int b2_unroll_packed(const uint64_t* lines, int64_t batch, int h, int w, int c, int kh, int kw, int stride, int pad,
+                     uint64_t* out, void* stream);
+
+/* layers.py:224-252 compute_correction from packed filter lines
+ * (filters, ceil(kh*kw*c/64)) -> corr (h_out*w_out, filters) int32. */
+int b2_conv_correction(const uint64_t* wwords, int64_t filters, int h, int w, int c, int kh, int kw, int stride,
+                       int pad, int32_t* corr, void* stream);
+
+/* layers.py:255-266 conv_forward / network.py:193-198 _PackedConv.run,
+ * batched, int32 output (batch, h_out, w_out, filters), correction added.
+ * `scratch` must hold batch*h_out*w_out*ceil(kh*kw*c/64) uint64 words when
+ * the implicit-im2col fast path does not apply (c % 32 != 0); pass NULL
+ * otherwise (b2_conv_scratch_words tells). */
+int64_t b2_conv_scratch_words(int64_t batch, int h, int w, int c, int kh, int kw, int stride, int pad);
+int b2_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const uint64_t* wwords,
+                    int64_t filters, int kh, int kw, int stride, int pad, const int32_t* corr, uint64_t* scratch,
+                    int32_t* out, void* stream);
+
+/* layers.py:265 / network.py:197 `acc += correction`, batched:
+ * acc[i] += corr[i % per_image] for i < n (corr broadcast over images). */
+int b2_add_correction_i32(int32_t* acc, const int32_t* corr, int64_t n, int64_t per_image, void* stream);
+
+/* Fused conv stage: implicit-im2col XOR-popc GEMM + correction +
+ * [2x2/2 max-pool when pool != 0] + batchnorm-threshold + sign + repack,
+ * i.e. network.py _PackedConv -> _Pool -> _PackedBN in one kernel.
+ * Requires c % 32 == 0 (site lines are whole uint32 words) and, with
+ * pool, even h_out/w_out.  out: (batch, sites_out, ceil(filters/64)) words.
+ * Returns B2_EINVAL when the shape is not eligible (use the unfused ops). */
+int b2_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, const uint64_t* wwords,
+                    int64_t filters, int kh, int kw, int stride, int pad, const int32_t* corr, int pool, b2_thresh th,
+                    uint64_t* out, void* stream);
+
+/* ---------------------------------------------------------------- epilogues */
+
+/* _kernels.py:224-240 maxpool on int32 (batch, h, w, c) -> (batch, ho, wo, c). */
+int b2_maxpool_i32(const int32_t* x, int64_t batch, int h, int w, int c, int ph, int pw, int stride, int32_t* out,
+                   void* stream);
+
+/* _kernels.py:243-267 threshold_sign_pack, batched; x (batch, sites, c) of
+ * dtype xkind (0 int32, 1 int64, 2 uint8).  flat=0: out (batch, sites,
+ * ceil(c/64)); flat=1: out (batch, ceil(sites*c/64)) in layout order. */
+int b2_threshold_pack(const void* x, int xkind, int64_t batch, int64_t sites, int64_t c, b2_thresh th, int flat,
+                      uint64_t* out, void* stream);
+
+/* _kernels.py:285-295 bn_affine: (double(x) - mean) * scale + beta, three
+ * separately rounded IEEE ops (no FMA), x (n) of xkind (0 int32, 1 int64,
+ * 3 float64), channel = i % c -> out (n) float64. */
+int b2_bn_affine_f64(const void* x, int xkind, int64_t n, const double* mean, const double* scale,
+                     const double* beta, int64_t c, double* out, void* stream);
+
+/* layers.py:137-191 BatchNormLayer: float64 scale = gamma/sqrt(var+eps) and
+ * the integer threshold by binary search (sentinels ALWAYS=-2^62,
+ * NEVER=2^62), on the device.  Inputs float32 (c); outputs scale64 (c)
+ * float64, thresh64 (c) int64, ge_dir (c) uint8, and thresh32 (c) int32 =
+ * clamp(thresh64, -(bound+1), bound+1). */
+int b2_bn_calibrate(const float* mean, const float* var, const float* gamma, const float* beta, double eps, int64_t c,
+                    int64_t bound, double* scale64, int64_t* thresh64, uint8_t* ge_dir, int32_t* thresh32,
+                    void* stream);
+
+/* ---------------------------------------------------------------- fused dense */
+
+/* network.py _PackedDense -> _PackedBN (flat): batched XOR-popc GEMM with
+ * fused threshold + repack.  x (batch, wpl) activation lines, w (units,
+ * wpl) -> out (batch, ceil(units/64)) packed words. */
+int b2_dense_bn_pack(const uint64_t* x, int64_t batch, const uint64_t* w, int64_t units, int64_t wpl, int32_t k,
+                     b2_thresh th, uint64_t* out, void* stream);
+
+/* network.py _PackedInput8 -> _PackedBN (flat): uint8 images (batch, k)
+ * -> bit-planes -> AND-popc GEMM -> threshold + repack, one kernel.
+ * w (units, ceil(k/64)) -> out (batch, ceil(units/64)). */
+int b2_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const uint64_t* w, int64_t units, b2_thresh th,
+                      uint64_t* out, void* stream);
+
+/* network.py _PackedByteBN (first-layer byte batchnorm) fused with the
+ * first conv (_PackedConv, kh*kw*c <= 32 bits per window) and its
+ * batchnorm (_PackedBN), one kernel: uint8 (batch, h, w, c) ->
+ * out (batch, h_out*w_out, ceil(filters/64)) words (filters <= 1024).
+ * Padding is handled by masking the out-of-bounds window bits, which equals
+ * the reference's pad-as--1 product plus its correction map exactly. */
+int b2_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
+                         const uint64_t* wwords, int64_t filters, int kh, int kw, int stride, int pad,
+                         b2_thresh th_out, uint64_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BITNN_B200_H */

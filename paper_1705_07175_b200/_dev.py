@@ -1,0 +1,86 @@
+"""Device-memory plumbing: torch CUDA tensors as buffers, ctypes pointers.
+
+PyTorch provides allocation, streams and graphs only; every computation on
+these buffers is one of our own kernels (see _lib.py).  Packed uint64
+words live in int64 tensors (same bytes).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_NP2T = {
+    np.dtype(np.uint64): torch.int64,
+    np.dtype(np.int64): torch.int64,
+    np.dtype(np.int32): torch.int32,
+    np.dtype(np.uint32): torch.int32,
+    np.dtype(np.uint8): torch.uint8,
+    np.dtype(np.float32): torch.float32,
+    np.dtype(np.float64): torch.float64,
+}
+_VIEW = {np.dtype(np.uint64): np.int64, np.dtype(np.uint32): np.int32}
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1705_07175_b200 runs on a CUDA GPU (sm_100a) only; there is no CPU fallback")
+
+
+def device() -> torch.device:
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def tdtype(np_dtype) -> torch.dtype:
+    return _NP2T[np.dtype(np_dtype)]
+
+
+def upload(arr: np.ndarray, dev=None) -> torch.Tensor:
+    arr = np.ascontiguousarray(arr)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    v = _VIEW.get(arr.dtype)
+    if v is not None:
+        arr = arr.view(v)
+    return torch.from_numpy(arr).to(dev or device())
+
+
+def empty(shape, np_dtype, dev=None) -> torch.Tensor:
+    return torch.empty(tuple(int(s) for s in shape), dtype=tdtype(np_dtype), device=dev or device())
+
+
+def zeros(shape, np_dtype, dev=None) -> torch.Tensor:
+    return torch.zeros(tuple(int(s) for s in shape), dtype=tdtype(np_dtype), device=dev or device())
+
+
+def download(t: torch.Tensor, np_dtype) -> np.ndarray:
+    a = t.detach().cpu().numpy()
+    np_dtype = np.dtype(np_dtype)
+    if a.dtype != np_dtype:
+        a = a.view(np_dtype)
+    return a
+
+
+def P(t) -> ctypes.c_void_p:
+    """Device pointer of a tensor (None -> NULL).
+
+    The tensor is kept alive until the next `_lib.call` returns, so a
+    temporary (`P(upload(x))`) cannot be freed and its memory handed to a
+    later argument before the kernel that reads it has been enqueued."""
+    if t is None:
+        return ctypes.c_void_p(0)
+    _lib.KEEPALIVE.append(t)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def sync():
+    torch.cuda.current_stream().synchronize()

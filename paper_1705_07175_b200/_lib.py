@@ -1,0 +1,102 @@
+"""ctypes binding of the C ABI in include/bitnn_b200.h.
+
+The CUDA library is the only compute path: there is no CPU fallback.  If
+lib/libbitnn_b200.so is missing this module raises at import time (build it
+with ``python -m paper_1705_07175_b200.build``); if no GPU is present, every
+op raises when it needs the device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .build import LIB
+
+if not os.path.exists(LIB):  # pragma: no cover - exercised on broken installs only
+    raise ImportError(f"CUDA library {LIB} is missing; run `python -m paper_1705_07175_b200.build` "
+                      "(this package has no CPU fallback)")
+
+_so = ctypes.CDLL(LIB)
+
+B2_EINVAL = 1000
+
+vp = ctypes.c_void_p
+i64 = ctypes.c_int64
+i32 = ctypes.c_int32
+cint = ctypes.c_int
+f64 = ctypes.c_double
+
+
+class Thresh(ctypes.Structure):
+    """struct b2_thresh (include/bitnn_b200.h)."""
+
+    _fields_ = [("thresh", vp), ("thresh64", vp), ("ge_dir", vp)]
+
+
+# name -> (restype, argtypes), in header order
+SIGNATURES = {
+    "b2_version": (ctypes.c_char_p, []),
+    "b2_launch_count": (i64, []),
+    "b2_pack_lines_f32": (cint, [vp, i64, i64, vp, vp]),
+    "b2_unpack_lines_f32": (cint, [vp, i64, i64, vp, vp]),
+    "b2_pack_byte_planes": (cint, [vp, i64, i64, vp, vp]),
+    "b2_bgemm": (cint, [vp, i64, vp, i64, i64, i32, vp, vp]),
+    "b2_bgemv": (cint, [vp, i64, i64, vp, i64, i32, vp, vp]),
+    "b2_bitplane_gemv": (cint, [vp, i64, vp, i64, i64, vp, vp]),
+    "b2_unroll_packed": (cint, [vp, i64, cint, cint, cint, cint, cint, cint, cint, vp, vp]),
+    "b2_conv_correction": (cint, [vp, i64, cint, cint, cint, cint, cint, cint, cint, vp, vp]),
+    "b2_conv_scratch_words": (i64, [i64, cint, cint, cint, cint, cint, cint, cint]),
+    "b2_conv_forward": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, vp, vp, vp, vp]),
+    "b2_add_correction_i32": (cint, [vp, vp, i64, i64, vp]),
+    "b2_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, vp, cint, Thresh, vp, vp]),
+    "b2_maxpool_i32": (cint, [vp, i64, cint, cint, cint, cint, cint, cint, vp, vp]),
+    "b2_threshold_pack": (cint, [vp, cint, i64, i64, i64, Thresh, cint, vp, vp]),
+    "b2_bn_affine_f64": (cint, [vp, cint, i64, vp, vp, vp, i64, vp, vp]),
+    "b2_bn_calibrate": (cint, [vp, vp, vp, vp, f64, i64, i64, vp, vp, vp, vp, vp]),
+    "b2_dense_bn_pack": (cint, [vp, i64, vp, i64, i64, i32, Thresh, vp, vp]),
+    "b2_input8_bn_pack": (cint, [vp, i64, i64, vp, i64, Thresh, vp, vp]),
+    "b2_byte_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, Thresh, vp, i64, cint, cint, cint, cint, Thresh, vp,
+                                    vp]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _fn = getattr(_so, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+class CudaOpError(RuntimeError):
+    pass
+
+
+# tensors whose pointers were taken for the call being assembled (see _dev.P)
+KEEPALIVE: list = []
+
+
+def call(name: str, *args) -> int:
+    try:
+        rc = getattr(_so, name)(*args)
+    finally:
+        KEEPALIVE.clear()
+    if rc != 0:
+        if rc == B2_EINVAL:
+            raise ValueError(f"{name}: invalid arguments for the CUDA kernel")
+        raise CudaOpError(f"{name} failed with cudaError {rc}")
+    return rc
+
+
+def raw(name: str):
+    return getattr(_so, name)
+
+
+def version() -> str:
+    return _so.b2_version().decode()
+
+
+def launch_count() -> int:
+    return int(_so.b2_launch_count())
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)

@@ -1,0 +1,701 @@
+"""Network runtime on the GPU (mirror of bitnn/network.py:1-588, packed backend).
+
+A model spec is validated exactly like the reference (`_compile`,
+network.py:331-486: same checks, same order, same "layer i: ..." messages),
+then planned into a short list of device stages.  Adjacent reference
+stages are fused where the layout allows it:
+
+    _PackedInput8 + _PackedBN            -> b2_input8_bn_pack
+    _PackedByteBN + _PackedConv + _PackedBN (window <= 32 bits)
+                                         -> b2_byte_conv_bn_pack
+    _PackedConv [+ _Pool 2x2/2] + _PackedBN (C % 32 == 0)
+                                         -> b2_conv_bn_pack
+    _PackedDense + _PackedBN             -> b2_dense_bn_pack
+    _FinalBN                             -> b2_bn_affine_f64
+
+and every other combination runs through the general kernels (unroll +
+bgemm + correction, maxpool, threshold-pack), all on the device.
+
+Every buffer is allocated at construction for `max_batch` images (the
+reference's Workspace, network.py:50-66); a forward pass performs no
+allocation and replays a CUDA graph captured per batch size.  `forward`
+keeps the reference's batch-1 contract and returns a reused host buffer;
+`forward_batch` runs any number of images.
+"""
+
+from __future__ import annotations
+
+import enum
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .layers import XKIND, _thresh_struct, calibrate_device, correction_device
+from .modelfile import (BatchNormRecord, ConvRecord, DenseRecord, Input8Record, MaxPoolRecord, ModelSpec,
+                        ModelValidationError, load_model, write_model)
+from .tensor import words_per_line
+
+MAX_K = 1 << 24
+
+
+class Backend(enum.Enum):
+    PACKED = "packed"
+    REFERENCE = "reference"
+
+
+def _wpl(bits):
+    return words_per_line(bits)
+
+
+# --------------------------------------------------------------------------- stages
+# Each stage owns its device output buffer for `cap` images; `src` is the
+# producing stage (None = network input bytes).  launch(batch) enqueues the
+# kernels for the first `batch` images on the current stream.
+
+
+class _Stage:
+    name = "stage"
+    out_dtype = np.uint64
+
+    def __init__(self, src):
+        self.src = src
+        self.out = None
+
+    def per_image(self):
+        raise NotImplementedError
+
+    def alloc(self, cap: int):
+        self.out = _dev.empty((cap, *self.per_image()), self.out_dtype)
+
+    def src_ptr(self, net):
+        return _dev.P(net._in if self.src is None else self.src.out)
+
+    def launches(self) -> int:
+        return 1
+
+
+class _Input8Fused(_Stage):
+    name = "input8+bn"
+
+    def __init__(self, src, rec, bn_dev):
+        super().__init__(src)
+        self.k, self.units = rec.input_len, rec.units
+        self.w = _dev.upload(rec.words)
+        self.bn = bn_dev
+
+    def per_image(self):
+        return (_wpl(self.units),)
+
+    def launch(self, net, batch, st):
+        _lib.call("b2_input8_bn_pack", self.src_ptr(net), batch, self.k, _dev.P(self.w), self.units,
+                  _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]), _dev.P(self.out), st)
+
+
+class _Input8Raw(_Stage):
+    name = "input8"
+    out_dtype = np.int64
+
+    def __init__(self, src, rec):
+        super().__init__(src)
+        self.k, self.units = rec.input_len, rec.units
+        self.w = _dev.upload(rec.words)
+
+    def per_image(self):
+        return (self.units,)
+
+    def alloc(self, cap):
+        super().alloc(cap)
+        self.planes = _dev.empty((8, cap, _wpl(self.k)), np.uint64)
+
+    def launch(self, net, batch, st):
+        _lib.call("b2_pack_byte_planes", self.src_ptr(net), batch, self.k, _dev.P(self.planes), st)
+        _lib.call("b2_bitplane_gemv", _dev.P(self.planes), batch, _dev.P(self.w), self.units, _wpl(self.k),
+                  _dev.P(self.out), st)
+
+    def launches(self):
+        return 2
+
+
+class _ByteConvFused(_Stage):
+    name = "bytebn+conv+bn"
+
+    def __init__(self, src, in_shape, bn0, rec, bn1):
+        super().__init__(src)
+        self.in_shape = in_shape
+        self.rec = rec
+        h, w, c = in_shape
+        self.h_out = (h + 2 * rec.pad - rec.kh) // rec.stride + 1
+        self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
+        self.w = _dev.upload(rec.words)
+        self.bn0, self.bn1 = bn0, bn1
+
+    def per_image(self):
+        return (self.h_out * self.w_out, _wpl(self.rec.filters))
+
+    def launch(self, net, batch, st):
+        h, w, c = self.in_shape
+        r = self.rec
+        _lib.call("b2_byte_conv_bn_pack", self.src_ptr(net), batch, h, w, c,
+                  _thresh_struct(self.bn0["thresh32"], self.bn0["thresh64"], self.bn0["ge"]), _dev.P(self.w),
+                  r.filters, r.kh, r.kw, r.stride, r.pad,
+                  _thresh_struct(self.bn1["thresh32"], self.bn1["thresh64"], self.bn1["ge"]), _dev.P(self.out), st)
+
+
+class _ConvFused(_Stage):
+    name = "conv+bn"
+
+    def __init__(self, src, in_shape, rec, pool: bool, bn_dev):
+        super().__init__(src)
+        self.in_shape, self.rec, self.pool, self.bn = in_shape, rec, pool, bn_dev
+        h, w, c = in_shape
+        self.h_out = (h + 2 * rec.pad - rec.kh) // rec.stride + 1
+        self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
+        self.w = _dev.upload(rec.words)
+        self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
+        if pool:
+            self.name = "conv+pool+bn"
+
+    def per_image(self):
+        sites = self.h_out * self.w_out // (4 if self.pool else 1)
+        return (sites, _wpl(self.rec.filters))
+
+    def launch(self, net, batch, st):
+        h, w, c = self.in_shape
+        r = self.rec
+        _lib.call("b2_conv_bn_pack", self.src_ptr(net), batch, h, w, c, _dev.P(self.w), r.filters, r.kh, r.kw,
+                  r.stride, r.pad, _dev.P(self.corr), int(self.pool),
+                  _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]), _dev.P(self.out), st)
+
+
+class _Conv(_Stage):
+    name = "conv"
+    out_dtype = np.int32
+
+    def __init__(self, src, in_shape, rec):
+        super().__init__(src)
+        self.in_shape, self.rec = in_shape, rec
+        h, w, c = in_shape
+        self.h_out = (h + 2 * rec.pad - rec.kh) // rec.stride + 1
+        self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
+        self.w = _dev.upload(rec.words)
+        self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
+
+    def per_image(self):
+        return (self.h_out, self.w_out, self.rec.filters)
+
+    def alloc(self, cap):
+        super().alloc(cap)
+        h, w, c = self.in_shape
+        r = self.rec
+        n = int(_lib.raw("b2_conv_scratch_words")(cap, h, w, c, r.kh, r.kw, r.stride, r.pad))
+        self.scratch = _dev.empty((n,), np.uint64) if n else None
+
+    def launch(self, net, batch, st):
+        h, w, c = self.in_shape
+        r = self.rec
+        _lib.call("b2_conv_forward", self.src_ptr(net), batch, h, w, c, _dev.P(self.w), r.filters, r.kh, r.kw,
+                  r.stride, r.pad, _dev.P(self.corr), _dev.P(self.scratch), _dev.P(self.out), st)
+
+    def launches(self):
+        return 3 if self.scratch is not None else 1
+
+
+class _Pool(_Stage):
+    name = "maxpool"
+    out_dtype = np.int32
+
+    def __init__(self, src, in_shape, rec):
+        super().__init__(src)
+        self.in_shape, self.rec = in_shape, rec
+        h, w, c = in_shape
+        self.out_shape = ((h - rec.ph) // rec.stride + 1, (w - rec.pw) // rec.stride + 1, c)
+
+    def per_image(self):
+        return self.out_shape
+
+    def launch(self, net, batch, st):
+        h, w, c = self.in_shape
+        _lib.call("b2_maxpool_i32", self.src_ptr(net), batch, h, w, c, self.rec.ph, self.rec.pw, self.rec.stride,
+                  _dev.P(self.out), st)
+
+
+class _BN(_Stage):
+    """Generic batchnorm + sign + pack (network.py:108-125 line plans)."""
+
+    name = "bn"
+
+    def __init__(self, src, dims, bn_dev, flat: bool, xkind: int):
+        super().__init__(src)
+        h, w, c = dims
+        sites = h * w
+        self.xkind = xkind
+        t64, ge = bn_dev["thresh64"], bn_dev["ge"]
+        if flat or sites == 1:
+            self.view, self.flat, self.lines, self.bits = (sites, c), True, 1, sites * c
+        elif c == 1:
+            self.view, self.flat, self.lines, self.bits = (h, w), False, h, w
+            t64, ge = t64[:1].expand(w).contiguous(), ge[:1].expand(w).contiguous()
+        else:
+            self.view, self.flat, self.lines, self.bits = (sites, c), False, sites, c
+        self.t64, self.ge = t64, ge
+
+    def per_image(self):
+        return (self.lines, _wpl(self.bits))
+
+    def launch(self, net, batch, st):
+        _lib.call("b2_threshold_pack", self.src_ptr(net), self.xkind, batch, self.view[0], self.view[1],
+                  _thresh_struct(None, self.t64, self.ge), int(self.flat), _dev.P(self.out), st)
+
+
+class _DenseFused(_Stage):
+    name = "dense+bn"
+
+    def __init__(self, src, rec, bn_dev):
+        super().__init__(src)
+        self.rec, self.bn = rec, bn_dev
+        self.w = _dev.upload(rec.words)
+
+    def per_image(self):
+        return (_wpl(self.rec.units),)
+
+    def launch(self, net, batch, st):
+        r = self.rec
+        _lib.call("b2_dense_bn_pack", self.src_ptr(net), batch, _dev.P(self.w), r.units, _wpl(r.input_len),
+                  r.input_len, _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]),
+                  _dev.P(self.out), st)
+
+
+class _Dense(_Stage):
+    name = "dense"
+    out_dtype = np.int32
+
+    def __init__(self, src, rec):
+        super().__init__(src)
+        self.rec = rec
+        self.w = _dev.upload(rec.words)
+
+    def per_image(self):
+        return (self.rec.units,)
+
+    def launch(self, net, batch, st):
+        r = self.rec
+        _lib.call("b2_bgemv", _dev.P(self.w), r.units, _wpl(r.input_len), self.src_ptr(net), batch, r.input_len,
+                  _dev.P(self.out), st)
+
+
+class _FinalBN(_Stage):
+    name = "final-bn"
+    out_dtype = np.float64
+
+    def __init__(self, src, bn_dev, classes: int, xkind: int):
+        super().__init__(src)
+        self.bn, self.classes, self.xkind = bn_dev, classes, xkind
+
+    def per_image(self):
+        return (self.classes,)
+
+    def launch(self, net, batch, st):
+        _lib.call("b2_bn_affine_f64", self.src_ptr(net), self.xkind, batch * self.classes, _dev.P(self.bn["mean64"]),
+                  _dev.P(self.bn["scale64"]), _dev.P(self.bn["beta64"]), self.classes, _dev.P(self.out), st)
+
+
+# --------------------------------------------------------------------------- network
+
+
+class Network:
+    """A model compiled for the GPU.  One instance per thread / stream."""
+
+    def __init__(self, spec: ModelSpec, backend=Backend.PACKED, layer_backends=None, max_batch: int = 1,
+                 use_graphs: bool = True):
+        if isinstance(backend, str):
+            backend = Backend(backend)
+        n_compute = sum(1 for r in spec.records if isinstance(r, (Input8Record, DenseRecord, ConvRecord)))
+        if layer_backends is None:
+            assigned = [backend] * n_compute
+        else:
+            assigned = [Backend(b) if isinstance(b, str) else b for b in layer_backends]
+            if len(assigned) != n_compute:
+                raise ModelValidationError(
+                    f"layer_backends needs one entry per weight layer ({n_compute}), got {len(assigned)}")
+        if any(b != Backend.PACKED for b in assigned):
+            raise NotImplementedError("only the packed backend exists on the GPU; the float reference backend "
+                                      "and hybrid mixes are out of scope (see DESIGN.md)")
+        self.spec = spec
+        self.input_dims = tuple(spec.input_dims)
+        self.backend = Backend.PACKED
+        self.layer_backends = assigned
+        self.use_graphs = use_graphs
+        ops, self.classes = self._validate(spec)
+        _dev.require_cuda()
+        self.device = _dev.device()
+        self.stages = self._plan(ops)
+        self.cap = 0
+        self._graphs = {}
+        self._reserve(max(1, int(max_batch)))
+        self._scores1 = None
+
+    # -- validation: network.py:331-486, same checks in the same order --------
+
+    def _validate(self, spec):
+        recs = spec.records
+        if not recs:
+            raise ModelValidationError("model has no layers")
+        if not isinstance(recs[-1], BatchNormRecord):
+            raise ModelValidationError(f"layer {len(recs) - 1}: model must end with a batchnorm score layer")
+        for i, r in enumerate(recs):
+            if isinstance(r, BatchNormRecord):
+                _check_bn_params(r, i)
+        ops = []
+        rep, shape = "bytes", self.input_dims
+        acc_kind = None
+
+        def consumer(i):
+            return recs[i + 1] if i + 1 < len(recs) else None
+
+        def want_flat(i):
+            return isinstance(consumer(i), (DenseRecord, Input8Record))
+
+        for i, rec in enumerate(recs):
+            last = i == len(recs) - 1
+            if isinstance(rec, Input8Record):
+                if i != 0:
+                    raise ModelValidationError(f"layer {i}: input8 is only valid as the first layer")
+                h, w, c = shape
+                if rec.input_len != h * w * c:
+                    raise ModelValidationError(
+                        f"layer {i}: input8 expects {rec.input_len} bytes but input dims give {h * w * c}")
+                ops.append(dict(kind="input8", rec=rec, i=i))
+                rep, shape, acc_kind = "acc", (1, 1, rec.units), ("input8", rec.input_len)
+            elif isinstance(rec, DenseRecord):
+                if rep not in ("packed", "float"):
+                    raise ModelValidationError(f"layer {i}: dense layer needs a signed activation input")
+                h, w, c = shape
+                if rec.input_len != h * w * c:
+                    raise ModelValidationError(
+                        f"layer {i}: dense expects {rec.input_len} inputs, previous layer gives {h * w * c}")
+                if h * w != 1:
+                    raise ModelValidationError(f"layer {i}: dense needs a flat activation line")
+                ops.append(dict(kind="dense", rec=rec, i=i))
+                rep, shape, acc_kind = "acc", (1, 1, rec.units), ("binary", rec.input_len)
+            elif isinstance(rec, ConvRecord):
+                if rep not in ("packed", "float") or shape[0] * shape[1] == 1:
+                    raise ModelValidationError(f"layer {i}: conv needs a spatial signed activation input")
+                h, w, c = shape
+                if c != rec.in_channels:
+                    raise ModelValidationError(
+                        f"layer {i}: conv expects {rec.in_channels} channels, previous layer gives {c}")
+                if h + 2 * rec.pad < rec.kh or w + 2 * rec.pad < rec.kw:
+                    raise ModelValidationError(f"layer {i}: kernel {rec.kh}x{rec.kw} larger than padded input")
+                if rec.k > MAX_K:
+                    raise ModelValidationError(f"layer {i}: dot length {rec.k} over limit {MAX_K}")
+                h_out = (h + 2 * rec.pad - rec.kh) // rec.stride + 1
+                w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
+                ops.append(dict(kind="conv", rec=rec, i=i, in_shape=shape, out_shape=(h_out, w_out, rec.filters)))
+                rep, shape, acc_kind = "acc", (h_out, w_out, rec.filters), ("binary", rec.k)
+            elif isinstance(rec, MaxPoolRecord):
+                if rep != "acc" or shape[0] * shape[1] == 1:
+                    raise ModelValidationError(f"layer {i}: maxpool needs spatial integer accumulators")
+                h, w, c = shape
+                if h < rec.ph or w < rec.pw:
+                    raise ModelValidationError(f"layer {i}: pooling window {rec.ph}x{rec.pw} larger than {h}x{w}")
+                out = ((h - rec.ph) // rec.stride + 1, (w - rec.pw) // rec.stride + 1, c)
+                ops.append(dict(kind="pool", rec=rec, i=i, in_shape=shape, out_shape=out))
+                shape = out
+            elif isinstance(rec, BatchNormRecord):
+                if i == 0:
+                    h, w, c = shape
+                    if rec.channels != c:
+                        raise ModelValidationError(f"layer {i}: batchnorm has {rec.channels} channels, input has {c}")
+                    if last:
+                        raise ModelValidationError("layer 0: model cannot be a lone batchnorm")
+                    flat = want_flat(i)
+                    ops.append(dict(kind="bytebn", rec=rec, i=i, dims=shape, flat=flat))
+                    rep = "packed"
+                    if flat:
+                        shape = (1, 1, h * w * c)
+                    continue
+                if rep != "acc":
+                    raise ModelValidationError(f"layer {i}: batchnorm needs accumulator input")
+                if rec.channels != shape[2]:
+                    raise ModelValidationError(
+                        f"layer {i}: batchnorm has {rec.channels} channels, previous layer gives {shape[2]}")
+                if last:
+                    if shape[0] * shape[1] != 1:
+                        raise ModelValidationError(f"layer {i}: final batchnorm must see a flat score vector")
+                    ops.append(dict(kind="final", rec=rec, i=i, acc=acc_kind))
+                    rep = "scores"
+                    continue
+                if not isinstance(consumer(i), (DenseRecord, ConvRecord)):
+                    raise ModelValidationError(f"layer {i}: batchnorm output has no consumer layer")
+                flat = want_flat(i)
+                ops.append(dict(kind="bn", rec=rec, i=i, dims=shape, flat=flat, acc=acc_kind))
+                rep = "packed"
+                if flat:
+                    shape = (1, 1, shape[0] * shape[1] * shape[2])
+            else:
+                raise ModelValidationError(f"layer {i}: unknown record {rec!r}")
+        if rep != "scores":
+            raise ModelValidationError("model does not end in a score-emitting batchnorm")
+        return ops, shape[2]
+
+    # -- planning: fuse adjacent reference stages into device kernels ---------
+
+    @staticmethod
+    def _bound(acc_kind) -> int:
+        kind, k = acc_kind
+        return 255 * k if kind == "input8" else k
+
+    def _plan(self, ops):
+        stages = []
+        src = None
+        j = 0
+        n = len(ops)
+
+        def cal(op, bound):
+            r = op["rec"]
+            return calibrate_device(r.mean, r.var, r.gamma, r.beta, r.eps, bound)
+
+        while j < n:
+            op = ops[j]
+            kind = op["kind"]
+            nxt = ops[j + 1] if j + 1 < n else None
+            nxt2 = ops[j + 2] if j + 2 < n else None
+            if kind == "input8":
+                r = op["rec"]
+                if nxt["kind"] == "bn" and 2 * _wpl(r.input_len) <= 128:
+                    st = _Input8Fused(src, r, cal(nxt, 255 * r.input_len))
+                    j += 2
+                else:
+                    st = _Input8Raw(src, r)
+                    j += 1
+            elif kind == "bytebn":
+                h, w, c = op["dims"]
+                conv = nxt if nxt is not None and nxt["kind"] == "conv" else None
+                if (conv is not None and not op["flat"] and conv["rec"].k <= 32 and 1 < conv["rec"].filters <= 1024
+                        and nxt2 is not None and nxt2["kind"] == "bn"
+                        and (not nxt2["flat"] or conv["rec"].filters % 64 == 0)):
+                    st = _ByteConvFused(src, op["dims"], cal(op, 255), conv["rec"], cal(nxt2, conv["rec"].k))
+                    j += 3
+                else:
+                    st = _BN(src, op["dims"], cal(op, 255), op["flat"], XKIND[np.dtype(np.uint8)])
+                    j += 1
+            elif kind == "conv":
+                r = op["rec"]
+                h, w, c = op["in_shape"]
+                ho, wo, f = op["out_shape"]
+                fusable_in = c % 32 == 0 and f > 1
+                pool_ok = (nxt is not None and nxt["kind"] == "pool" and (nxt["rec"].ph, nxt["rec"].pw,
+                                                                          nxt["rec"].stride) == (2, 2, 2)
+                           and ho % 2 == 0 and wo % 2 == 0 and nxt2 is not None and nxt2["kind"] == "bn")
+                if fusable_in and nxt is not None and nxt["kind"] == "bn" and (not nxt["flat"] or f % 64 == 0):
+                    st = _ConvFused(src, op["in_shape"], r, False, cal(nxt, r.k))
+                    j += 2
+                elif fusable_in and pool_ok and (not nxt2["flat"] or f % 64 == 0):
+                    st = _ConvFused(src, op["in_shape"], r, True, cal(nxt2, r.k))
+                    j += 3
+                else:
+                    st = _Conv(src, op["in_shape"], r)
+                    j += 1
+            elif kind == "pool":
+                st = _Pool(src, op["in_shape"], op["rec"])
+                j += 1
+            elif kind == "bn":
+                xk = XKIND[np.dtype(np.int64 if op["acc"][0] == "input8" else np.int32)]
+                st = _BN(src, op["dims"], cal(op, self._bound(op["acc"])), op["flat"], xk)
+                j += 1
+            elif kind == "dense":
+                r = op["rec"]
+                if nxt["kind"] == "bn":
+                    st = _DenseFused(src, r, cal(nxt, r.input_len))
+                    j += 2
+                else:
+                    st = _Dense(src, r)
+                    j += 1
+            elif kind == "final":
+                xk = XKIND[np.dtype(np.int64 if op["acc"][0] == "input8" else np.int32)]
+                st = _FinalBN(src, cal(op, 0), op["rec"].channels, xk)
+                j += 1
+            else:  # pragma: no cover
+                raise AssertionError(kind)
+            stages.append(st)
+            src = st
+        return stages
+
+    # -- workspace / execution ---------------------------------------------------
+
+    @property
+    def input_len(self) -> int:
+        h, w, c = self.input_dims
+        return h * w * c
+
+    def _reserve(self, cap: int):
+        if cap <= self.cap:
+            return
+        self._graphs.clear()
+        self._in = _dev.empty((cap, self.input_len), np.uint8)
+        for st in self.stages:
+            st.alloc(cap)
+        self._in_host = torch.empty((cap, self.input_len), dtype=torch.uint8, pin_memory=True)
+        self._out_host = torch.empty((cap, self.classes), dtype=torch.float64, pin_memory=True)
+        self._in_host_np = self._in_host.numpy()
+        self._out_host_np = self._out_host.numpy()
+        self.cap = cap
+        self._scores1 = None
+
+    @property
+    def scores_device(self):
+        return self.stages[-1].out
+
+    @property
+    def input_device(self):
+        return self._in
+
+    @property
+    def workspace_bytes(self) -> int:
+        tot = self._in.numel()
+        for st in self.stages:
+            for t in (st.out, getattr(st, "planes", None), getattr(st, "scratch", None)):
+                if t is not None:
+                    tot += t.numel() * t.element_size()
+        return tot
+
+    def launches_per_forward(self) -> int:
+        return sum(st.launches() for st in self.stages)
+
+    def _launch_all(self, batch: int):
+        st = _dev.stream()
+        for s in self.stages:
+            s.launch(self, batch, st)
+
+    def run(self, batch: int):
+        """Enqueue the forward pass of the first `batch` images already in
+        `input_device` on the current stream (scores land in `scores_device`)."""
+        if batch > self.cap:
+            raise ValueError(f"batch {batch} exceeds workspace capacity {self.cap}")
+        if batch <= 0:
+            return
+        if not self.use_graphs:
+            self._launch_all(batch)
+            return
+        g = self._graphs.get(batch)
+        if g is None:
+            self._launch_all(batch)  # eager warm-up (module load, attributes)
+            torch.cuda.current_stream().synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch_all(batch)
+            self._graphs[batch] = g
+        g.replay()
+
+    def forward_host(self, images: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """(N, input_len) uint8 host images -> (N, classes) float64 scores."""
+        n = images.shape[0]
+        if out is None:
+            out = np.empty((n, self.classes), dtype=np.float64)
+        s = torch.cuda.current_stream()
+        for b0 in range(0, n, self.cap):
+            b = min(self.cap, n - b0)
+            self._in_host_np[:b] = images[b0:b0 + b]
+            self._in[:b].copy_(self._in_host[:b], non_blocking=True)
+            self.run(b)
+            self._out_host[:b].copy_(self.scores_device[:b], non_blocking=True)
+            s.synchronize()
+            out[b0:b0 + b] = self._out_host_np[:b]
+        return out
+
+
+def _check_bn_params(r: BatchNormRecord, i: int):
+    """BatchNormLayer.__init__ checks (layers.py:119-130), raised as the reference's ValueError."""
+    mean, var, gamma, beta = (np.atleast_1d(np.asarray(v, dtype=np.float32)) for v in (r.mean, r.var, r.gamma,
+                                                                                      r.beta))
+    if not (mean.shape == var.shape == gamma.shape == beta.shape) or mean.ndim != 1:
+        raise ValueError("batchnorm parameter vectors must share one length")
+    if np.any(var < 0):
+        raise ValueError("negative variance")
+    if r.eps < 0:
+        raise ValueError("negative epsilon")
+    if np.any(var.astype(np.float64) + r.eps <= 0):
+        raise ValueError("variance + epsilon must be positive")
+    if not all(np.all(np.isfinite(v)) for v in (mean, var, gamma, beta)):
+        raise ValueError("non-finite batchnorm parameter")
+
+
+def load(path, backend=Backend.PACKED, layer_backends=None, max_batch: int = 1) -> Network:
+    return Network(load_model(path), backend, layer_backends, max_batch=max_batch)
+
+
+def _check_image(net: Network, image) -> np.ndarray:
+    x = np.asarray(image)
+    if x.dtype != np.uint8:
+        raise ValueError(f"expected uint8 input, got {x.dtype}")
+    h, w, c = net.input_dims
+    if x.shape != (h, w, c) and x.shape != (h * w * c,):
+        raise ValueError(f"expected input shape {(h, w, c)} or ({h * w * c},), got {x.shape}")
+    if not x.flags.c_contiguous:
+        raise ValueError("input must be C-contiguous")
+    return x
+
+
+def forward(net: Network, image: np.ndarray) -> np.ndarray:
+    """One image -> its float64 score vector.  Like the reference the result
+    lives in the network's (pinned host) workspace and is overwritten by the
+    next call; the same array object is returned every time."""
+    x = _check_image(net, image)
+    net._in_host_np[0] = x.reshape(-1)
+    net._in[:1].copy_(net._in_host[:1], non_blocking=True)
+    net.run(1)
+    net._out_host[:1].copy_(net.scores_device[:1], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    if net._scores1 is None:
+        net._scores1 = net._out_host_np[0]
+    return net._scores1
+
+
+def forward_batch(net: Network, images: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+    """N images (N, H, W, C) or (N, H*W*C) uint8 -> (N, classes) float64 scores."""
+    x = np.asarray(images)
+    if x.dtype != np.uint8:
+        raise ValueError(f"expected uint8 input, got {x.dtype}")
+    h, w, c = net.input_dims
+    if x.ndim < 1 or (x.shape[1:] != (h, w, c) and x.shape[1:] != (h * w * c,)):
+        raise ValueError(f"expected input shape (N, {h}, {w}, {c}) or (N, {h * w * c}), got {x.shape}")
+    x = np.ascontiguousarray(x).reshape(x.shape[0], -1)
+    return net.forward_host(x, out)
+
+
+def classify(net: Network, image: np.ndarray) -> int:
+    return int(np.argmax(forward(net, image)))
+
+
+def classify_batch(net: Network, images: np.ndarray) -> np.ndarray:
+    return np.argmax(forward_batch(net, images), axis=1)
+
+
+def convert(net: Network, target) -> Network:
+    if isinstance(target, str):
+        target = Backend(target)
+    if target != Backend.PACKED:
+        raise NotImplementedError("the float reference backend is out of scope on the GPU (see DESIGN.md)")
+    return Network(net.spec, Backend.PACKED, max_batch=net.cap)
+
+
+def serialize(net: Network) -> bytes:
+    return write_model(net.spec)
+
+
+def model_size(obj) -> dict:
+    """Serialized parameter bytes per representation (network.py:562-588)."""
+    spec = obj.spec if isinstance(obj, Network) else obj
+    packed_w = ref_w = bn = 0
+    for rec in spec.records:
+        if isinstance(rec, (Input8Record, DenseRecord)):
+            packed_w += rec.words.nbytes
+            ref_w += 4 * rec.units * rec.input_len
+        elif isinstance(rec, ConvRecord):
+            packed_w += rec.words.nbytes
+            ref_w += 4 * rec.filters * rec.k
+        elif isinstance(rec, BatchNormRecord):
+            bn += 4 * (4 * rec.channels + 1)
+    return {"reference": ref_w + bn, "packed": packed_w + bn, "reference_weights": ref_w,
+            "packed_weights": packed_w, "batchnorm_bytes": bn}
