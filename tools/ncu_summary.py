@@ -1,0 +1,64 @@
+"""Summarise ncu reports / launch lists into profiles/ (run in the build container).
+
+    python tools/ncu_summary.py launches gpurun_out/launches.csv > profiles/xxx_launches.md
+    python tools/ncu_summary.py full gpurun_out/prof.ncu-rep > profiles/xxx_full.md
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_alu_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread", "launch__grid_size",
+        "launch__block_size", "smsp__cycles_active.avg", "sm__cycles_elapsed.avg.per_second",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+
+
+def launches(path):
+    lines = open(path).read().splitlines()
+    start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    agg = defaultdict(lambda: [0, 0.0])
+    order = []
+    for r in rows:
+        name = r.get("Kernel Name", "?")
+        try:
+            v = float(r["Metric Value"].replace(",", ""))
+        except (KeyError, ValueError):
+            continue
+        unit = r.get("Metric Unit", "")
+        us = v / 1e3 if unit in ("ns", "nsecond") else (v * 1e3 if unit in ("ms", "msecond") else v)
+        if name not in agg:
+            order.append(name)
+        agg[name][0] += 1
+        agg[name][1] += us
+    tot = sum(a[1] for a in agg.values())
+    print("| kernel | launches | total us | share |\n|---|---|---|---|")
+    for n in sorted(order, key=lambda n: -agg[n][1]):
+        c, us = agg[n]
+        print(f"| `{n[:110]}` | {c} | {us:.1f} | {100 * us / tot:.1f}% |")
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:
+        print(f"### `{vals[hdr.index('Kernel Name')][:160]}`\n")
+        print("| metric | value | unit |\n|---|---|---|")
+        for k in KEYS:
+            for i, h in enumerate(hdr):
+                if h.endswith(k):
+                    print(f"| {h} | {vals[i]} | {units[i]} |")
+                    break
+        print()
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
