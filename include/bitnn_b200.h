@@ -173,6 +173,60 @@ int b2_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b
                          const uint64_t* wwords, int64_t filters, int kh, int kw, int stride, int pad,
                          b2_thresh th_out, uint64_t* out, void* stream);
 
+/* ---------------------------------------------------------------- tensor-core path
+ *
+ * The same operators on the 5th-generation tensor cores (tcgen05.mma
+ * kind::i8): a bit encodes +1/-1, so popc-XOR dot products are int8 dot
+ * products of +/-1 bytes with 0 for every element outside the operand
+ * (padding), computed exactly in int32.  Activations stay bit-packed in HBM
+ * and are widened on chip; weights are widened once (b2_expand_i8).  See
+ * DESIGN.md "tensor-core binary GEMM".  Zero padding makes the reference's
+ * correction map (layers.py:224-252) implicit: conv results already equal
+ * conv_forward's "bgemm + correction". */
+
+/* K rounded up to the 128-element block of the tcgen05 int8 GEMM. */
+int64_t b2_i8_kpad(int64_t k);
+
+/* Widen packed +/-1 lines to int8 for the tensor pipe (_kernels.py:57-64
+ * unpack_lines semantics, signed bytes): w (rows, wpl) with k valid bits ->
+ * out (rows, b2_i8_kpad(k)) int8, +1 / -1 for k' < k and 0 for the padding.
+ * permute=1: K order permuted inside each 32-group to match the on-chip
+ * widening of packed A operands (all bit-packed entry points below);
+ * permute=0: natural K order (b2_tc_input8_bn_pack, whose A is raw bytes). */
+int b2_expand_i8(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, int permute, int8_t* out, void* stream);
+
+/* _kernels.py:85-106 bgemm_packed: a (m, wpl) packed rows, b_i8 =
+ * b2_expand_i8(permute=1) of the (n, wpl) packed columns -> out (m, n) int32
+ * = k - 2*popc(a_m XOR b_n). */
+int b2_tc_bgemm(const uint64_t* a, int64_t m, const int8_t* b_i8, int64_t n, int64_t wpl, int32_t k, int32_t* out,
+                void* stream);
+
+/* network.py _PackedDense -> _PackedBN (flat), as b2_dense_bn_pack. */
+int b2_tc_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl, int32_t k,
+                        b2_thresh th, uint64_t* out, void* stream);
+
+/* layers.py:255-266 conv_forward (correction included), implicit bit-im2col,
+ * batched; requires c % 64 == 0.  out (batch, h_out, w_out, filters) int32. */
+int b2_tc_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
+                       int64_t filters, int kh, int kw, int stride, int pad, int32_t* out, void* stream);
+
+/* _PackedConv [-> _Pool 2x2/2] -> _PackedBN, as b2_conv_bn_pack; c % 64 == 0. */
+int b2_tc_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
+                       int64_t filters, int kh, int kw, int stride, int pad, int pool, b2_thresh th, uint64_t* out,
+                       void* stream);
+
+/* _PackedInput8 -> _PackedBN (flat): uint8 (batch, k) x +/-1 weights
+ * (b2_expand_i8 permute=0) = the bit-plane sum of gemm.py:120-146 exactly,
+ * then threshold + repack; k % 4 == 0. */
+int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_t* w_i8, int64_t units, b2_thresh th,
+                         uint64_t* out, void* stream);
+
+/* _PackedByteBN -> _PackedConv (kh*kw*c <= 128) [-> _Pool 2x2/2] ->
+ * _PackedBN, as b2_byte_conv_bn_pack. */
+int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
+                            const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
+                            b2_thresh th_out, uint64_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,3 +84,13 @@ def stream() -> ctypes.c_void_p:
 
 def sync():
     torch.cuda.current_stream().synchronize()
+
+
+def widen_i8(words: torch.Tensor, rows: int, k: int, permute: bool = True) -> torch.Tensor:
+    """Packed +/-1 rows (rows, wpl) on the device -> int8 (rows, kpad) for the
+    tensor-core GEMM (b2_expand_i8)."""
+    kpad = int(_lib.raw("b2_i8_kpad")(int(k)))
+    out = torch.empty((int(rows), kpad), dtype=torch.int8, device=words.device)
+    wpl = (int(k) + 63) // 64
+    _lib.call("b2_expand_i8", P(words), int(rows), wpl, int(k), int(bool(permute)), P(out), stream())
+    return out

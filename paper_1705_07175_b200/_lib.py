@@ -58,7 +58,24 @@ SIGNATURES = {
     "b2_input8_bn_pack": (cint, [vp, i64, i64, vp, i64, Thresh, vp, vp]),
     "b2_byte_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, Thresh, vp, i64, cint, cint, cint, cint, Thresh, vp,
                                     vp]),
+    "b2_i8_kpad": (i64, [i64]),
+    "b2_expand_i8": (cint, [vp, i64, i64, i64, cint, vp, vp]),
+    "b2_tc_bgemm": (cint, [vp, i64, vp, i64, i64, i32, vp, vp]),
+    "b2_tc_dense_bn_pack": (cint, [vp, i64, vp, i64, i64, i32, Thresh, vp, vp]),
+    "b2_tc_conv_forward": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, vp, vp]),
+    "b2_tc_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, cint, Thresh, vp, vp]),
+    "b2_tc_input8_bn_pack": (cint, [vp, i64, i64, vp, i64, Thresh, vp, vp]),
+    "b2_tc_byte_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, Thresh, vp, i64, cint, cint, cint, cint, cint,
+                                       Thresh, vp, vp]),
 }
+
+# GEMM engine for the shapes both engines support: "tc" (tcgen05 int8 tensor
+# cores, the default) or "popc" (LOP3+POPC on the CUDA cores).  The choice
+# is measured, not a fallback: DESIGN.md "engine choice" and
+# profiles/ hold the ncu evidence; B2_ENGINE=popc exists to reproduce it.
+ENGINE = os.environ.get("B2_ENGINE", "tc")
+if ENGINE not in ("tc", "popc"):  # pragma: no cover
+    raise ValueError(f"B2_ENGINE must be 'tc' or 'popc', got {ENGINE!r}")
 
 for _name, (_res, _args) in SIGNATURES.items():
     _fn = getattr(_so, _name)

@@ -1,0 +1,670 @@
+// Binary GEMM on the 5th-generation tensor cores (tcgen05 kind::i8, sm_100a).
+//
+// The XNOR-popcount dot product of the reference
+//     dot = K - 2 * popc(a XOR b)                     (_kernels.py:85-106)
+// is the integer inner product of the +/-1 vectors the bits encode, so the
+// GEMM runs exactly on the int8 tensor pipe once each bit is widened to a
+// signed byte (+1 -> 0x01, -1 -> 0xFF) and every element that lies OUTSIDE
+// the operand (conv padding sites, K beyond the line) is the byte 0:
+//
+//   * activations stay bit-packed in HBM (the reference's layout, 1 bit per
+//     element); producer warps gather one 128-bit K block per row (implicit
+//     bit-im2col for convolutions), widen it in registers and store the 128
+//     bytes straight into TENSOR MEMORY with tcgen05.st — the MMA reads A
+//     from TMEM, so the widened operand never touches shared memory;
+//   * weights are widened once at load (b2_expand_i8) to int8 rows padded
+//     to a multiple of 128 with zeros and streamed by TMA (128B swizzle)
+//     into a shared-memory ring;
+//   * one thread issues tcgen05.mma (M=128, N=BN, K=32 per instruction)
+//     into a double-buffered int32 accumulator in TMEM;
+//   * epilogue warps tcgen05.ld the accumulator (thread = output row) and
+//     apply the reference's stage chain in registers: int32 store, or
+//     batchnorm threshold + sign + repack into channel-fastest words, or
+//     2x2 max-pool + threshold + repack (rows ordered pool-window-major so
+//     the four rows of a window are four adjacent lanes).
+//
+// Zero bytes for padding make the correction map of the reference
+// (layers.py:224-252, added in network.py:193-198) unnecessary: the
+// reference's "pad as -1 then add correction" IS the zero-padded product.
+//
+// Warp roles (512 threads, one persistent CTA per SM, 512 TMEM columns):
+//   warp 0      TMA producer for B (one lane)
+//   warp 1      MMA issuer (one lane)
+//   warp 2      TMEM allocator
+//   warps 4-11  A producers (warp%4 = TMEM lane quarter = row quarter;
+//               warps 4-7 widen K bits 0-63 of a block, 8-11 bits 64-127)
+//   warps 12-15 epilogue     (same lane-quarter rule)
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace b2 {
+namespace tc {
+
+constexpr int BM = 128;                 // tile rows = TMEM lanes
+constexpr int BK = 128;                 // int8 K per stage = one 128-byte swizzle atom
+constexpr int STAGES_MAX = 8;           // smem B ring and TMEM A ring depth (BN <= 128)
+constexpr int A_STAGE_COLS = BK / 4;    // 32 TMEM columns per A stage
+constexpr int NUM_THREADS = 512;
+constexpr int PF = 4;                   // A-producer prefetch depth (K blocks)
+
+enum AMode { A_ROWS = 0, A_CONV = 1, A_BYTES = 2, A_BYTECONV = 3 };
+enum EMode { E_I32 = 0, E_PACK = 1, E_POOLPACK = 2 };
+
+struct Args {
+  // ---- A operand
+  const uint32_t* a;  // packed rows / NHWC-bits activations / bytes (as words)
+  int64_t lda;        // A_ROWS/A_BYTES: uint32 words per row
+  int awords;         // A_ROWS: valid uint32 words per row (ceil(K/32)); A_BYTES: valid bytes per row (K)
+  // conv geometry (A_CONV: spw = C/32 words per site; A_BYTECONV: c = channels)
+  int H, W, spw, sstride, kh, kw, stride, pad, Ho, Wo, c;
+  const int32_t* in_thresh;  // A_BYTECONV: byte batchnorm thresholds (per channel)
+  const uint8_t* in_ge;
+  // ---- problem
+  int64_t M;
+  int N;
+  int nkb;  // K blocks of 128
+  // ---- epilogue
+  int32_t* out_i32;
+  int64_t ldo;
+  uint32_t* out_bits;
+  int64_t ldo32;
+  const int32_t* thresh;
+  const uint8_t* ge;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Same wait for roles that idle for long stretches (epilogue, TMA issue):
+// back off so their polling does not steal issue slots from the producers.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t done;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(ns);
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+#define B2_R32(v)                                                                                                   \
+  "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),    \
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),   \
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),   \
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+#define B2_W32(v)                                                                                                   \
+  "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),      \
+      "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),        \
+      "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),       \
+      "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+
+// 32 consecutive TMEM columns of this thread's lane <- v[0..31]
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      B2_R32(v)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : B2_W32(v)
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// K-major operand, 128-byte swizzle: 8-row atoms of 128 B, atoms 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// instruction descriptor: D s32, A s8|u8, B s8, both K-major, M = 128
+__host__ __device__ constexpr uint32_t idesc_i8(int n, bool a_unsigned) {
+  return (2u << 4) | ((a_unsigned ? 0u : 1u) << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+// 32 bits (elements k..k+31, LSB first) -> 32 signed bytes in 8 words,
+// bit 1 -> +1 (0x01), bit 0 -> -1 (0xFF); an invalid (padding) word -> 0.
+// K is PERMUTED inside each 32-element group: byte j of output word s holds
+// element 8j + s, so each output word is one shift, one mask and one IMAD.
+// The weights are widened with the same permutation (k_expand_i8); a dot
+// product is invariant under a common permutation of K.
+__device__ __forceinline__ void widen32(uint32_t x, bool ok, uint32_t* o) {
+  const uint32_t nx = ok ? ~x : 0u;
+  const uint32_t c = ok ? 0x01010101u : 0u;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = ((nx >> q) & 0x01010101u) * 0xFEu + c;
+}
+__host__ __device__ __forceinline__ int perm_pos(int k) {  // element k of a 32-group -> byte position
+  return 4 * (k & 7) + (k >> 3);
+}
+
+// Output row -> (image, oy, ox); pool-ordered rows put each 2x2 window in
+// four consecutive rows: m = 4*q + 2*cy + cx.
+template <bool POOLED>
+__device__ __forceinline__ void row_pos(const Args& g, int64_t m, int64_t& img, int& oy, int& ox) {
+  if constexpr (POOLED) {
+    int64_t q = m >> 2;
+    int cell = (int)(m & 3);
+    int hp = g.Ho >> 1, wp = g.Wo >> 1;
+    img = q / (hp * wp);
+    int r = (int)(q - img * (hp * wp));
+    oy = 2 * (r / wp) + (cell >> 1);
+    ox = 2 * (r % wp) + (cell & 1);
+  } else {
+    int64_t hw = (int64_t)g.Ho * g.Wo;
+    img = m / hw;
+    int r = (int)(m - img * hw);
+    oy = r / g.Wo;
+    ox = r % g.Wo;
+  }
+}
+
+// Per-bit-masked variant for the byte-batchnorm first layer: bits whose
+// valid bit is 0 (window cells in the padding ring) become the byte 0.
+__device__ __forceinline__ void widen32m(uint32_t x, uint32_t valid, uint32_t* o) {
+  const uint32_t nx = ~x & valid;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = ((nx >> q) & 0x01010101u) * 0xFEu + ((valid >> q) & 0x01010101u);
+}
+
+// Gather cursor of one A-producer thread (one tile row, one half of each
+// 128-element K block): walks this CTA's (tile, K block) sequence.
+//   A_ROWS / A_CONV / A_BYTECONV: 64 packed bits (uint2) + validity
+//   A_BYTES:                      64 raw bytes (4 x uint4)
+template <int AM, bool POOLED>
+struct ACursor {
+  int64_t t;       // tile of the next fetch
+  int kb;          // K block of the next fetch
+  bool mok;        // row inside M
+  const uint32_t* base;
+  int iy0, ix0;    // conv: window origin of this row
+  int cell, within, dy, dx;  // conv: window cell and word of this half's next K words
+  int64_t img;
+
+  __device__ __forceinline__ void tile_setup(const Args& g, int64_t mtiles, int64_t tiles, int r, int half) {
+    kb = 0;
+    const int64_t m = (t % mtiles) * BM + r;
+    mok = t < tiles && m < g.M;
+    if constexpr (AM == A_CONV || AM == A_BYTECONV) {
+      img = 0;
+      int oy = 0, ox = 0;
+      if (mok) row_pos<POOLED>(g, m, img, oy, ox);
+      iy0 = oy * g.stride - g.pad;
+      ix0 = ox * g.stride - g.pad;
+      if constexpr (AM == A_CONV) {
+        base = g.a + img * (int64_t)g.H * g.W * g.sstride;
+        cell = dy = dx = 0;
+        within = 2 * half;
+        while (within >= g.spw) within -= g.spw, step_cell(g);
+      }
+    } else {
+      base = g.a + (mok ? m : 0) * g.lda;
+    }
+  }
+  __device__ __forceinline__ void step_cell(const Args& g) {
+    ++cell;
+    if (++dx == g.kw) dx = 0, ++dy;
+  }
+  __device__ __forceinline__ void start(const Args& g, int64_t t0, int64_t mtiles, int64_t tiles, int r, int half) {
+    t = t0;
+    tile_setup(g, mtiles, tiles, r, half);
+  }
+  __device__ __forceinline__ void advance(const Args& g, int64_t step, int64_t mtiles, int64_t tiles, int r,
+                                          int half) {
+    if (++kb == g.nkb) {
+      t += step;
+      tile_setup(g, mtiles, tiles, r, half);
+    } else if constexpr (AM == A_CONV) {
+      within += 4;
+      while (within >= g.spw) within -= g.spw, step_cell(g);
+    }
+  }
+
+  // packed-bit modes: x = 64 bits of K, vm = validity (all ones / zero, or
+  // per bit for A_BYTECONV)
+  __device__ __forceinline__ void fetch_bits(const Args& g, int half, uint2& x, uint2& vm) {
+    x = make_uint2(0, 0);
+    vm = make_uint2(0, 0);
+    if constexpr (AM == A_ROWS) {
+      const int w0 = kb * 4 + 2 * half;
+      if (mok) {
+        vm = make_uint2(~0u, ~0u);
+        const uint32_t* p = base + w0;
+        if (w0 + 2 <= g.awords && (g.lda & 1) == 0) {
+          x = __ldg(reinterpret_cast<const uint2*>(p));
+        } else {
+          if (w0 + 0 < g.awords) x.x = __ldg(p + 0);
+          if (w0 + 1 < g.awords) x.y = __ldg(p + 1);
+        }
+      }
+    } else if constexpr (AM == A_CONV) {
+      // two consecutive K words of one site (spw even)
+      const int iy = iy0 + dy, ix = ix0 + dx;
+      if (mok && dy < g.kh && iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) {
+        vm = make_uint2(~0u, ~0u);
+        x = __ldg(reinterpret_cast<const uint2*>(base + ((int64_t)iy * g.W + ix) * g.sstride + within));
+      }
+    } else if constexpr (AM == A_BYTECONV) {
+      // byte batchnorm (network.py:128-138) of the window's bytes, K order
+      // (dy, dx, c) with c fastest (layers.py:3-8); padding cells invalid
+      if (mok && kb == 0) {
+        const int kbits = g.kh * g.kw * g.c;
+        const int lo = 64 * half, hi = kbits < lo + 64 ? kbits : lo + 64;
+        const uint8_t* xi = reinterpret_cast<const uint8_t*>(g.a) + img * (int64_t)g.H * g.W * g.c;
+        uint64_t bits = 0, valid = 0;
+        for (int p = lo; p < hi; ++p) {
+          const int cellp = p / g.c, ch = p - cellp * g.c;
+          const int iy = iy0 + cellp / g.kw, ix = ix0 + cellp % g.kw;
+          if (iy < 0 || iy >= g.H || ix < 0 || ix >= g.W) continue;
+          const int32_t v = __ldg(xi + ((int64_t)iy * g.W + ix) * g.c + ch);
+          const bool b = thr_bit(v, __ldg(g.in_thresh + ch), __ldg(g.in_ge + ch) != 0);
+          bits |= (uint64_t)b << (p - lo);
+          valid |= 1ull << (p - lo);
+        }
+        x = make_uint2((uint32_t)bits, (uint32_t)(bits >> 32));
+        vm = make_uint2((uint32_t)valid, (uint32_t)(valid >> 32));
+      }
+    }
+  }
+  // A_BYTES: bytes [128 kb + 64 half, +64) of the row (awords = valid words)
+  __device__ __forceinline__ void fetch_bytes(const Args& g, int half, uint4 (&x)[4]) {
+    const int w0 = kb * 32 + 16 * half;
+    const bool vec = (g.lda & 3) == 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[i] = make_uint4(0, 0, 0, 0);
+      const int w = w0 + 4 * i;
+      if (!mok || w >= g.awords) continue;
+      if (vec && w + 4 <= g.awords) {
+        x[i] = __ldg(reinterpret_cast<const uint4*>(base + w));
+      } else {  // row tail or a row pitch that is not 16-byte aligned
+        x[i].x = __ldg(base + w);
+        if (w + 1 < g.awords) x[i].y = __ldg(base + w + 1);
+        if (w + 2 < g.awords) x[i].z = __ldg(base + w + 2);
+        if (w + 3 < g.awords) x[i].w = __ldg(base + w + 3);
+      }
+    }
+  }
+};
+
+template <int BN>
+constexpr int stages() {
+  return BN <= 128 ? STAGES_MAX : 6;  // 6 x 32 KB B stages at BN = 256
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// ------------------------------------------------------------------ kernel
+template <int BN, int AM, int EM>
+__global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap, const Args g) {
+  constexpr bool POOLED = (EM == E_POOLPACK);
+  constexpr int B_STAGE_BYTES = BN * BK;
+  constexpr int STAGES = stages<BN>();
+  constexpr int ACC_COLS = BN;
+  constexpr int ACC_BUFS = BN <= 128 ? 2 : 1;  // accumulator double buffer when TMEM allows
+  constexpr int A_COL0 = ACC_BUFS * ACC_COLS;
+  static_assert(A_COL0 + STAGES * A_STAGE_COLS <= 512, "TMEM budget");
+  constexpr uint32_t IDESC = idesc_i8(BN, AM == A_BYTES);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sb = smem;                                                      // STAGES x B_STAGE_BYTES
+  int4* sthr = reinterpret_cast<int4*>(smem + STAGES * B_STAGE_BYTES);     // BN/2 x (mul, add, mul, add)
+  uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + BN / 2);              // BN/32 ge-direction masks
+  uint64_t* full = reinterpret_cast<uint64_t*>(sgm + 8);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t mtiles = (g.M + BM - 1) / BM;
+  const int ntiles = (g.N + BN - 1) / BN;
+  const int64_t tiles = mtiles * ntiles;  // tile t -> (m tile t % mtiles, n tile t / mtiles)
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 8 + 1);  // 8 A-producer warps + the TMA expect_tx arrival
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (B)
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int n0 = (int)(t / mtiles) * BN;
+        for (int kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait_sleep(&empty[s], ph ^ 1, 64);
+          mbar_expect_tx(&full[s], B_STAGE_BYTES);
+          tma_load_2d(sb + s * B_STAGE_BYTES, &bmap, &full[s], kb * BK, n0);
+          if (++s == STAGES) s = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * ACC_COLS;
+        for (int kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
+          const uint32_t bs = smem_u32(sb + s * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k)
+            tc_mma_i8(d, a + k * 8, sw128_desc(bs + k * 32), IDESC, (kb | k) ? 1u : 0u);
+          tc_commit(&empty[s]);
+          if (++s == STAGES) s = 0, ph ^= 1;
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ------------------------------------------------ A producers
+    // Two warps per TMEM lane quarter, each producing half (64 elements) of
+    // the row's 128-element K block.  The cursor runs PF K blocks ahead of
+    // the stage being written (across tile boundaries), so the global
+    // gathers overlap the widening and the TMEM stores; each stage is
+    // published one iteration later, after its tcgen05.st has drained.
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int r = q * 32 + lane;  // tile row = TMEM lane
+    const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / 2);
+    ACursor<AM, POOLED> cur;
+    cur.start(g, blockIdx.x, mtiles, tiles, r, half);
+    const int64_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t jobs = my_tiles * g.nkb;
+    int s = 0, pending = -1;
+    uint32_t ph = 0;
+    auto publish = [&](int stage, uint32_t (&v)[16]) {
+      if (pending >= 0) {
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[pending]);
+      }
+      mbar_wait(&empty[stage], ph ^ 1);
+      tc_fence_after();
+#ifndef B2_PROBE_SKIP_A
+      tmem_st16(st_addr + stage * A_STAGE_COLS, v);
+#endif
+      pending = stage;
+    };
+    if constexpr (AM == A_BYTES) {
+      uint4 qx[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        cur.fetch_bytes(g, half, qx[u]);
+        cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+      }
+      for (int64_t j0 = 0; j0 < jobs; j0 += 2) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (j0 + u < jobs) {
+            uint32_t v[16];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              v[4 * i + 0] = qx[u][i].x;
+              v[4 * i + 1] = qx[u][i].y;
+              v[4 * i + 2] = qx[u][i].z;
+              v[4 * i + 3] = qx[u][i].w;
+            }
+            cur.fetch_bytes(g, half, qx[u]);
+            cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+            publish(s, v);
+            if (++s == STAGES) s = 0, ph ^= 1;
+          }
+        }
+      }
+    } else {
+      uint2 qx[PF], qv[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        cur.fetch_bits(g, half, qx[u], qv[u]);
+        cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+      }
+      for (int64_t j0 = 0; j0 < jobs; j0 += PF) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          if (j0 + u < jobs) {
+            uint32_t v[16];
+#ifndef B2_PROBE_SKIP_A
+            if constexpr (AM == A_BYTECONV) {
+              widen32m(qx[u].x, qv[u].x, v + 0);
+              widen32m(qx[u].y, qv[u].y, v + 8);
+            } else {
+              widen32(qx[u].x, qv[u].x != 0, v + 0);
+              widen32(qx[u].y, qv[u].y != 0, v + 8);
+            }
+#endif
+            // refill the slot only after it was consumed: the load lands in
+            // the same registers and nothing waits on it until PF stages later
+            cur.fetch_bits(g, half, qx[u], qv[u]);
+            cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+            publish(s, v);
+            if (++s == STAGES) s = 0, ph ^= 1;
+          }
+        }
+      }
+    }
+    if (pending >= 0) {
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[pending]);
+    }
+  } else if (warp >= 12) {
+    // ------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int64_t m = (t % mtiles) * BM + r;
+      const int n0 = (int)(t / mtiles) * BN;
+      const bool mok = m < g.M;
+      if constexpr (EM != E_I32) {
+        // this tile's thresholds as bit = (acc * mul + add >= 0):
+        // ge -> (1, -t), le -> (-1, t), column beyond N -> (0, -1) = bit 0
+        epi_bar();
+        int* st = reinterpret_cast<int*>(sthr);
+        for (int j = r; j < BN; j += 128) {
+          const int n = n0 + j;
+          int mul = 0, add = -1;
+          if (n < g.N) {
+            const int32_t th = __ldg(g.thresh + n);
+            const bool ge = __ldg(g.ge + n) != 0;
+            mul = ge ? 1 : -1;
+            add = ge ? -th : th;
+          }
+          st[2 * j] = mul;
+          st[2 * j + 1] = add;
+        }
+        if (r < BN / 32) {
+          uint32_t gmw = 0;
+          for (int j = 0; j < 32; ++j) {
+            const int n = n0 + 32 * r + j;
+            gmw |= (uint32_t)(n >= g.N || __ldg(g.ge + n) != 0) << j;
+          }
+          sgm[r] = gmw;
+        }
+        epi_bar();
+      }
+      mbar_wait_sleep(&tfull[acc], aph, 256);
+      tc_fence_after();
+      uint32_t words[BN / 32];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_addr + acc * ACC_COLS + c * 32, v);
+        tmem_wait_ld();
+        const int nb = n0 + c * 32;
+        if constexpr (EM == E_I32) {
+          if (mok && nb < g.N) {
+            int32_t* o = g.out_i32 + m * g.ldo + nb;
+            if (nb + 32 <= g.N && ((g.ldo & 3) == 0)) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<int4*>(o + j) = make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < g.N) o[j] = (int)v[j];
+            }
+          }
+        } else {
+          // sign bits of acc * mul + add, MSB first, then reversed
+          uint32_t sg = 0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const int4 p = sthr[c * 16 + j / 2];
+            const int d0 = (int)v[j] * p.x + p.y;
+            const int d1 = (int)v[j + 1] * p.z + p.w;
+            sg = __funnelshift_l((uint32_t)d0, sg, 1);
+            sg = __funnelshift_l((uint32_t)d1, sg, 1);
+          }
+          uint32_t w = ~__brev(sg);
+          if constexpr (EM == E_POOLPACK) {
+            // max over the 2x2 window then threshold == OR (ge) / AND (le)
+            // of the four thresholded rows (monotone threshold)
+            const uint32_t gm = sgm[c];
+            uint32_t o = w | __shfl_xor_sync(0xffffffffu, w, 1);
+            o |= __shfl_xor_sync(0xffffffffu, o, 2);
+            uint32_t a = w & __shfl_xor_sync(0xffffffffu, w, 1);
+            a &= __shfl_xor_sync(0xffffffffu, a, 2);
+            w = (o & gm) | (a & ~gm);
+          }
+          words[c] = w;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if constexpr (EM != E_I32) {
+        const int64_t site = POOLED ? (m >> 2) : m;
+        const bool writer = mok && (!POOLED || (lane & 3) == 0);
+        if (writer) {
+          uint32_t* o = g.out_bits + site * g.ldo32 + n0 / 32;
+          if (n0 / 32 + BN / 32 <= g.ldo32 && (g.ldo32 & 3) == 0) {
+#pragma unroll
+            for (int c = 0; c < BN / 32; c += 4)
+              *reinterpret_cast<uint4*>(o + c) = make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c)
+              if (n0 / 32 + c < g.ldo32) o[c] = words[c];
+          }
+        }
+      }
+      if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int BN>
+constexpr int smem_bytes() {
+  return stages<BN>() * BN * BK + BN * 8 + 32 + 8 * (2 * stages<BN>() + 4) + 16 + 1024;
+}
+
+}  // namespace tc
+}  // namespace b2

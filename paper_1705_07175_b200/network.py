@@ -83,11 +83,18 @@ class _Input8Fused(_Stage):
         self.k, self.units = rec.input_len, rec.units
         self.w = _dev.upload(rec.words)
         self.bn = bn_dev
+        self.tc = _lib.ENGINE == "tc" and self.k % 4 == 0
+        # bytes x +/-1 weights in natural K order (the u8 operand is not widened)
+        self.w8 = _dev.widen_i8(self.w, self.units, self.k, permute=False) if self.tc else None
 
     def per_image(self):
         return (_wpl(self.units),)
 
     def launch(self, net, batch, st):
+        if self.tc and batch >= TC_MIN_ROWS:
+            _lib.call("b2_tc_input8_bn_pack", self.src_ptr(net), batch, self.k, _dev.P(self.w8), self.units,
+                      _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]), _dev.P(self.out), st)
+            return
         _lib.call("b2_input8_bn_pack", self.src_ptr(net), batch, self.k, _dev.P(self.w), self.units,
                   _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]), _dev.P(self.out), st)
 
@@ -129,6 +136,10 @@ class _ByteConvFused(_Stage):
         self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
         self.w = _dev.upload(rec.words)
         self.bn0, self.bn1 = bn0, bn1
+        self.tc = _lib.ENGINE == "tc" and rec.k <= 128
+        if not self.tc and (rec.k > 32 or rec.filters > 1024):
+            raise AssertionError("planner chose the fused byte conv for an ineligible shape")
+        self.w8 = _dev.widen_i8(self.w, rec.filters, rec.k) if self.tc else None
 
     def per_image(self):
         return (self.h_out * self.w_out, _wpl(self.rec.filters))
@@ -136,6 +147,12 @@ class _ByteConvFused(_Stage):
     def launch(self, net, batch, st):
         h, w, c = self.in_shape
         r = self.rec
+        if self.tc:
+            _lib.call("b2_tc_byte_conv_bn_pack", self.src_ptr(net), batch, h, w, c,
+                      _thresh_struct(self.bn0["thresh32"], self.bn0["thresh64"], self.bn0["ge"]), _dev.P(self.w8),
+                      r.filters, r.kh, r.kw, r.stride, r.pad, 0,
+                      _thresh_struct(self.bn1["thresh32"], self.bn1["thresh64"], self.bn1["ge"]), _dev.P(self.out), st)
+            return
         _lib.call("b2_byte_conv_bn_pack", self.src_ptr(net), batch, h, w, c,
                   _thresh_struct(self.bn0["thresh32"], self.bn0["thresh64"], self.bn0["ge"]), _dev.P(self.w),
                   r.filters, r.kh, r.kw, r.stride, r.pad,
@@ -152,7 +169,11 @@ class _ConvFused(_Stage):
         self.h_out = (h + 2 * rec.pad - rec.kh) // rec.stride + 1
         self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
         self.w = _dev.upload(rec.words)
-        self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
+        self.tc = _lib.ENGINE == "tc" and c % 64 == 0
+        if self.tc:  # zero padding on the tensor cores: no correction map needed
+            self.w8, self.corr = _dev.widen_i8(self.w, rec.filters, rec.k), None
+        else:
+            self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
         if pool:
             self.name = "conv+pool+bn"
 
@@ -163,6 +184,11 @@ class _ConvFused(_Stage):
     def launch(self, net, batch, st):
         h, w, c = self.in_shape
         r = self.rec
+        if self.tc:
+            _lib.call("b2_tc_conv_bn_pack", self.src_ptr(net), batch, h, w, c, _dev.P(self.w8), r.filters, r.kh,
+                      r.kw, r.stride, r.pad, int(self.pool),
+                      _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]), _dev.P(self.out), st)
+            return
         _lib.call("b2_conv_bn_pack", self.src_ptr(net), batch, h, w, c, _dev.P(self.w), r.filters, r.kh, r.kw,
                   r.stride, r.pad, _dev.P(self.corr), int(self.pool),
                   _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]), _dev.P(self.out), st)
@@ -179,7 +205,11 @@ class _Conv(_Stage):
         self.h_out = (h + 2 * rec.pad - rec.kh) // rec.stride + 1
         self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
         self.w = _dev.upload(rec.words)
-        self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
+        self.tc = _lib.ENGINE == "tc" and c % 64 == 0
+        if self.tc:
+            self.w8, self.corr = _dev.widen_i8(self.w, rec.filters, rec.k), None
+        else:
+            self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
 
     def per_image(self):
         return (self.h_out, self.w_out, self.rec.filters)
@@ -188,12 +218,16 @@ class _Conv(_Stage):
         super().alloc(cap)
         h, w, c = self.in_shape
         r = self.rec
-        n = int(_lib.raw("b2_conv_scratch_words")(cap, h, w, c, r.kh, r.kw, r.stride, r.pad))
+        n = 0 if self.tc else int(_lib.raw("b2_conv_scratch_words")(cap, h, w, c, r.kh, r.kw, r.stride, r.pad))
         self.scratch = _dev.empty((n,), np.uint64) if n else None
 
     def launch(self, net, batch, st):
         h, w, c = self.in_shape
         r = self.rec
+        if self.tc:
+            _lib.call("b2_tc_conv_forward", self.src_ptr(net), batch, h, w, c, _dev.P(self.w8), r.filters, r.kh,
+                      r.kw, r.stride, r.pad, _dev.P(self.out), st)
+            return
         _lib.call("b2_conv_forward", self.src_ptr(net), batch, h, w, c, _dev.P(self.w), r.filters, r.kh, r.kw,
                   r.stride, r.pad, _dev.P(self.corr), _dev.P(self.scratch), _dev.P(self.out), st)
 
@@ -248,6 +282,12 @@ class _BN(_Stage):
                   _thresh_struct(None, self.t64, self.ge), int(self.flat), _dev.P(self.out), st)
 
 
+# Below this many activation rows a dense layer is a weight stream (GEMV on
+# the packed weights, 8x fewer HBM bytes than int8); above it the tensor
+# cores win.
+TC_MIN_ROWS = 64
+
+
 class _DenseFused(_Stage):
     name = "dense+bn"
 
@@ -255,12 +295,18 @@ class _DenseFused(_Stage):
         super().__init__(src)
         self.rec, self.bn = rec, bn_dev
         self.w = _dev.upload(rec.words)
+        self.w8 = _dev.widen_i8(self.w, rec.units, rec.input_len) if _lib.ENGINE == "tc" else None
 
     def per_image(self):
         return (_wpl(self.rec.units),)
 
     def launch(self, net, batch, st):
         r = self.rec
+        if self.w8 is not None and batch >= TC_MIN_ROWS:
+            _lib.call("b2_tc_dense_bn_pack", self.src_ptr(net), batch, _dev.P(self.w8), r.units, _wpl(r.input_len),
+                      r.input_len, _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]),
+                      _dev.P(self.out), st)
+            return
         _lib.call("b2_dense_bn_pack", self.src_ptr(net), batch, _dev.P(self.w), r.units, _wpl(r.input_len),
                   r.input_len, _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]),
                   _dev.P(self.out), st)
@@ -472,7 +518,8 @@ class Network:
             elif kind == "bytebn":
                 h, w, c = op["dims"]
                 conv = nxt if nxt is not None and nxt["kind"] == "conv" else None
-                if (conv is not None and not op["flat"] and conv["rec"].k <= 32 and 1 < conv["rec"].filters <= 1024
+                kmax, fmax = (128, 1 << 30) if _lib.ENGINE == "tc" else (32, 1024)
+                if (conv is not None and not op["flat"] and conv["rec"].k <= kmax and 1 < conv["rec"].filters <= fmax
                         and nxt2 is not None and nxt2["kind"] == "bn"
                         and (not nxt2["flat"] or conv["rec"].filters % 64 == 0)):
                     st = _ByteConvFused(src, op["dims"], cal(op, 255), conv["rec"], cal(nxt2, conv["rec"].k))

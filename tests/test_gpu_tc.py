@@ -1,0 +1,188 @@
+"""GPU parity of the tensor-core (tcgen05 kind::i8) entry points against the
+CPU oracle: plain GEMM (ragged K, tails in M and N, both tile widths),
+implicit-im2col convolutions (padding 0-2, stride 1-2, 1x1..5x5, channel
+counts 64..512, int32 and fused threshold/pool/pack epilogues), dense,
+byte-input first layers, and whole networks with both engines."""
+
+import numpy as np
+import pytest
+
+from paper_1705_07175_b200 import _dev, _lib, forward_batch, gemm, layers, zoo
+from paper_1705_07175_b200.layers import BatchNormLayer
+from paper_1705_07175_b200.network import Network
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_pm1(rng, *shape):
+    return np.where(rng.random(shape) < 0.5, -1.0, 1.0).astype(np.float32)
+
+
+def rand_bn(rng, c, spread):
+    return BatchNormLayer(rng.standard_normal(c) * spread, rng.random(c) * 5 + 1, rng.standard_normal(c),
+                          rng.standard_normal(c))
+
+
+def th(cal):
+    return layers._thresh_struct(cal["thresh32"], cal["thresh64"], cal["ge"])
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (5, 3, 63), (128, 128, 128), (129, 127, 129), (300, 200, 300),
+                                   (64, 257, 1000), (1000, 333, 4096), (257, 1024, 1152), (100, 64, 16384),
+                                   (513, 300, 2304)])
+def test_tc_bgemm_vs_oracle(oracle, m, n, k):
+    rng = np.random.default_rng(m * 7 + n * 13 + k)
+    a = oracle.pack_lines(rand_pm1(rng, m, k))
+    b = oracle.pack_lines(rand_pm1(rng, n, k))
+    got = gemm.bgemm_device(_dev.upload(a), m, _dev.upload(b), n, a.shape[1], k, engine="tc")
+    assert np.array_equal(_dev.download(got, np.int32), oracle.bgemm(a, b, k))
+
+
+def test_tc_and_popc_engines_agree():
+    rng = np.random.default_rng(11)
+    for m, n, k in ((2048, 512, 4608), (777, 129, 65)):
+        a = _dev.upload(zoo.pack_bits_host(rng.random((m, k)) >= 0.5))
+        b = _dev.upload(zoo.pack_bits_host(rng.random((n, k)) >= 0.5))
+        wpl = -(-k // 64)
+        tc = _dev.download(gemm.bgemm_device(a, m, b, n, wpl, k, engine="tc"), np.int32)
+        pc = _dev.download(gemm.bgemm_device(a, m, b, n, wpl, k, engine="popc"), np.int32)
+        assert np.array_equal(tc, pc), (m, n, k)
+
+
+CONV_CASES = [  # h, w, c, f, kh, kw, stride, pad, batch
+    (8, 8, 128, 128, 3, 3, 1, 1, 3), (6, 10, 64, 96, 3, 3, 1, 1, 2), (16, 16, 256, 256, 3, 3, 1, 1, 2),
+    (8, 8, 512, 64, 3, 3, 1, 1, 2), (7, 9, 64, 10, 5, 5, 2, 2, 2), (5, 5, 128, 300, 1, 1, 1, 0, 3),
+    (9, 7, 192, 40, 3, 2, 2, 0, 2), (4, 4, 512, 512, 3, 3, 1, 1, 4), (3, 3, 64, 17, 3, 3, 1, 2, 1)]
+
+
+@pytest.mark.parametrize("h,w,c,f,kh,kw,stride,pad,batch", CONV_CASES)
+def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batch):
+    rng = np.random.default_rng(h * 31 + c + f)
+    xs = np.stack([oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)])
+    wt = oracle.pack_lines(rand_pm1(rng, f, kh * kw * c))
+    corr = oracle.compute_correction(wt, (h, w, c), (kh, kw), stride, pad)
+    ho, wo = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
+    want = np.stack([oracle.bgemm(oracle.unroll_packed(x, h, w, c, kh, kw, stride, pad), wt, kh * kw * c) + corr
+                     for x in xs]).reshape(batch, ho, wo, f)
+    wd = _dev.upload(wt)
+    w8 = _dev.widen_i8(wd, f, kh * kw * c)
+    out = _dev.empty((batch, ho, wo, f), np.int32)
+    _lib.call("b2_tc_conv_forward", _dev.P(_dev.upload(xs)), batch, h, w, c, _dev.P(w8), f, kh, kw, stride, pad,
+              _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.int32), want)
+
+
+@pytest.mark.parametrize("h,w,c,f,pool,batch", [(8, 8, 128, 128, True, 3), (6, 10, 64, 96, False, 2),
+                                                (16, 16, 256, 256, True, 2), (8, 8, 512, 64, False, 2),
+                                                (4, 4, 512, 512, True, 5), (32, 32, 128, 128, True, 2),
+                                                (6, 6, 64, 200, True, 3)])
+def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch):
+    rng = np.random.default_rng(5 + h + c + f)
+    xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
+    wt = oracle.pack_lines(rand_pm1(rng, f, 9 * c))
+    bn = rand_bn(rng, f, 20.0)
+    bn.gamma[::7] = 0.0  # ALWAYS / NEVER sentinels
+    bn.gamma[3::11] *= -1
+    bn = BatchNormLayer(bn.mean, bn.var, bn.gamma, bn.beta)
+    corr = oracle.compute_correction(wt, (h, w, c), (3, 3), 1, 1)
+    want = []
+    for x in xs:
+        acc = (oracle.bgemm(oracle.unroll_packed(x, h, w, c, 3, 3, 1, 1), wt, 9 * c) + corr).reshape(h, w, f)
+        if pool:
+            acc = oracle.maxpool(acc, 2, 2, 2)
+        want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn.thresh, bn.ge_dir, False))
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 9 * c)
+    wd = _dev.upload(wt)
+    w8 = _dev.widen_i8(wd, f, 9 * c)
+    sites = h * w // (4 if pool else 1)
+    out = _dev.empty((batch, sites, -(-f // 64)), np.uint64)
+    _lib.call("b2_tc_conv_bn_pack", _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1,
+              int(pool), th(cal), _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
+
+
+@pytest.mark.parametrize("batch,units,k", [(1, 300, 4096), (5, 64, 1000), (37, 1024, 8192), (200, 4096, 4096),
+                                           (129, 10, 1024), (300, 130, 300), (64, 1000, 784)])
+def test_tc_dense_bn_pack_vs_oracle(oracle, batch, units, k):
+    rng = np.random.default_rng(batch + units + k)
+    x = oracle.pack_lines(rand_pm1(rng, batch, k))
+    wt = oracle.pack_lines(rand_pm1(rng, units, k))
+    bn = rand_bn(rng, units, 30.0)
+    acc = oracle.bgemm(x, wt, k)
+    want = np.stack([oracle.threshold_sign_pack(acc[i].reshape(1, -1), bn.thresh, bn.ge_dir, True)[0]
+                     for i in range(batch)])
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, k)
+    w8 = _dev.widen_i8(_dev.upload(wt), units, k)
+    out = _dev.empty((batch, -(-units // 64)), np.uint64)
+    _lib.call("b2_tc_dense_bn_pack", _dev.P(_dev.upload(x)), batch, _dev.P(w8), units, -(-k // 64), k, th(cal),
+              _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), want)
+
+
+@pytest.mark.parametrize("batch,units,k", [(64, 4096, 784), (300, 100, 784), (129, 256, 12), (70, 64, 1024)])
+def test_tc_input8_bn_pack_vs_oracle(oracle, batch, units, k):
+    rng = np.random.default_rng(batch * units + k)
+    u = rng.integers(0, 256, (batch, k), dtype=np.uint8)
+    u[0] = 255
+    wt = oracle.pack_lines(rand_pm1(rng, units, k))
+    bn = rand_bn(rng, units, 5000.0)
+    want = []
+    for i in range(batch):
+        y = oracle.bitplane_matvec(oracle.pack_byte_planes(u[i].reshape(1, -1))[:, 0, :], wt)
+        want.append(oracle.threshold_sign_pack(y.reshape(1, -1), bn.thresh, bn.ge_dir, True)[0])
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 255 * k)
+    w8 = _dev.widen_i8(_dev.upload(wt), units, k, permute=False)
+    out = _dev.empty((batch, -(-units // 64)), np.uint64)
+    _lib.call("b2_tc_input8_bn_pack", _dev.P(_dev.upload(u)), batch, k, _dev.P(w8), units, th(cal), _dev.P(out),
+              _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
+
+
+@pytest.mark.parametrize("h,w,c,f,kh,pad,stride,pool", [(32, 32, 3, 128, 3, 1, 1, False), (16, 12, 3, 64, 3, 1, 1, True),
+                                                        (9, 9, 4, 200, 5, 2, 2, False), (8, 8, 14, 32, 3, 1, 1, True),
+                                                        (5, 7, 1, 10, 3, 0, 1, False)])
+def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, pool):
+    rng = np.random.default_rng(h * w + c + f)
+    batch = 3
+    imgs = rng.integers(0, 256, (batch, h, w, c), dtype=np.uint8)
+    bn0 = rand_bn(rng, c, 100.0)
+    k = kh * kh * c
+    wt = oracle.pack_lines(rand_pm1(rng, f, k))
+    bn1 = rand_bn(rng, f, 8.0)
+    corr = oracle.compute_correction(wt, (h, w, c), (kh, kh), stride, pad)
+    ho, wo = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kh) // stride + 1
+    want = []
+    for i in range(batch):
+        if c == 1:  # single-channel maps are per-row lines (tensor.py:165-173, network.py:121-124)
+            lines = oracle.threshold_sign_pack(imgs[i].reshape(h, w).astype(np.int64), np.repeat(bn0.thresh, w),
+                                               np.repeat(bn0.ge_dir, w), False)
+        else:
+            lines = oracle.threshold_sign_pack(imgs[i].reshape(h * w, c).astype(np.int64), bn0.thresh, bn0.ge_dir,
+                                               False)
+        acc = (oracle.bgemm(oracle.unroll_packed(lines, h, w, c, kh, kh, stride, pad), wt, k) + corr)
+        acc = acc.reshape(ho, wo, f)
+        if pool:
+            acc = oracle.maxpool(acc, 2, 2, 2)
+        want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn1.thresh, bn1.ge_dir, False))
+    cal0 = layers.calibrate_device(bn0.mean, bn0.var, bn0.gamma, bn0.beta, bn0.eps, 255)
+    cal1 = layers.calibrate_device(bn1.mean, bn1.var, bn1.gamma, bn1.beta, bn1.eps, k)
+    w8 = _dev.widen_i8(_dev.upload(wt), f, k)
+    sites = ho * wo // (4 if pool else 1)
+    out = _dev.empty((batch, sites, -(-f // 64)), np.uint64)
+    _lib.call("b2_tc_byte_conv_bn_pack", _dev.P(_dev.upload(imgs)), batch, h, w, c, th(cal0), _dev.P(w8), f, kh, kh,
+              stride, pad, int(pool), th(cal1), _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
+
+
+@pytest.mark.parametrize("name", ["bcnn", "bmlp"])
+def test_network_engines_agree(networks_golden, name, monkeypatch):
+    spec = zoo.bcnn_spec() if name == "bcnn" else zoo.bmlp_spec()
+    imgs = networks_golden[f"{name}_images"]
+    want = networks_golden[f"{name}_scores"]
+    reps = 300 // imgs.shape[0] + 1  # > TC_MIN_ROWS so the dense layers take the tensor-core path
+    batch = np.concatenate([imgs] * reps)
+    for engine in ("tc", "popc"):
+        monkeypatch.setattr(_lib, "ENGINE", engine)
+        net = Network(spec, max_batch=batch.shape[0])
+        got = forward_batch(net, batch)
+        assert np.array_equal(got, np.concatenate([want] * reps)), engine
