@@ -17,8 +17,10 @@ timings).  Multi-GPU runs are launched with torchrun, one rank per GPU.
            uint8 images: pinned H2D copy + forward + D2H of the scores inside
            the timed region.
 `roofline` — per-stage device times (CUDA events, eager launches on the
-           same stream), dominant stage's achieved bit-op/s against the
-           measured POPC-pipe peak of this B200.
+           same stream); the dominant stage's achieved ops/s (2 per binary
+           MAC) against the int8 tensor-core peak measured on this GPU in the
+           same run (cuBLASLt int8 GEMM); the measured POPC-pipe peak is
+           reported beside it.
 `cpu_baseline` — the CPU oracle port of the reference (oracle/, OpenMP
            threads where the reference uses numba prange) on a bounded
            sample, rank 0 only.
@@ -59,33 +61,49 @@ def env_int(name, default):
 # --------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line).
+
+    Started before the warm-up so the first sample exists when timing
+    begins; `mark()` brackets the timed region and `summary()` keeps the
+    samples taken inside it (each line is timestamped on arrival)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 20):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            deadline = time.time() + 5.0
+            while not self.lines and time.time() < deadline:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(2 * self.period_ms / 1e3)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -93,9 +111,16 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = self.t1 if self.t1 is not None else time.time()
+        inside = [ln for ts, ln in self.lines if t0 <= ts <= t1 + self.period_ms / 1e3]
+        where = "timed region"
+        if not inside and self.lines:  # region shorter than one sampling period: nearest sample
+            inside = [min(self.lines, key=lambda x: abs(x[0] - t0))[1]]
+            where = "nearest sample to a timed region shorter than the sampling period"
+        sm, mx, reasons = [], [], set()
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) != 6:
                 continue
@@ -110,7 +135,35 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": where}
+
+
+def measure_int8_peak(dev, n: int = 8192, reps: int = 10):
+    """Dense int8 tensor-core peak of THIS GPU, measured: cuBLASLt int8 GEMM
+    (torch._int_mm, int32 accumulate) on n^3, best of `reps`, CUDA events.
+    The binary GEMM counts 2 ops per binary MAC; on the tensor pipe one
+    binary MAC is one int8 MAC, so the units match (TOP/s)."""
+    import torch
+    try:
+        a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev)
+        b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev).t().contiguous().t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * n ** 3 / (best / 1e3) / 1e12, f"cuBLASLt int8 GEMM (torch._int_mm) {n}^3, best of {reps}, this GPU"
+    except Exception as exc:  # pragma: no cover - library without int8 GEMM
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return 2.0 * peaks["bf16_tflops"], f"2 x measured bf16 ({peaks['bf16_tflops']} TF/s, MEASURED_PEAKS.json); " \
+                                           f"torch._int_mm unavailable: {exc}"
 
 
 # --------------------------------------------------------------------------- workloads
@@ -204,21 +257,22 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (also captures the CUDA graph for batch B)
-    for _ in range(max(args.warmup, 1)):
-        net.run(B)
-    barrier()
-
     launches0 = _lib.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
+        # warm-up (also captures the CUDA graph for batch B)
+        for _ in range(max(args.warmup, 1)):
+            net.run(B)
         barrier()
+        launches0 = _lib.launch_count()
+        clk.mark(True)
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             ev[i][0].record(stream)
             net.run(B)
             ev[i][1].record(stream)
         barrier()
+        clk.mark(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -263,25 +317,48 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         stages.append({"stage": st.name, "ms": a.elapsed_time(b) / reps, "bitops": 2 * stage_macs(st) * B})
     stage_total = sum(s["ms"] for s in stages)
-    dom = max(stages, key=lambda s: s["ms"])
-    achieved = dom["bitops"] / (dom["ms"] / 1e3) / 1e12
+    int8_peak, int8_src = measure_int8_peak(dev)
+    for s_ in stages:
+        s_["tops"] = s_["bitops"] / (s_["ms"] / 1e3) / 1e12 if s_["ms"] > 0 else 0.0
+        s_["frac_of_int8_peak"] = s_["tops"] / int8_peak
+    dom = max(stages, key=lambda s_: s_["ms"])
+    achieved = dom["tops"]
+    traffic = stage_traffic(args.workload, dom["stage"], stages.index(dom))
     result = {
         "metric": BASELINE_METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64-packed bits / int32 acc / f64 scores", "data": "synthetic",
-        "config": config_dict(args) | {"global_batch": B * world},
+        "vs_baseline": None, "dtype": "u1 packed (+/-1) activations, s8 tensor-core operands, s32 acc, f64 scores",
+        "data": "synthetic",
+        "config": config_dict(args) | {"global_batch": B * world, "engine": _lib.ENGINE},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": int(host_imgs.nbytes),
                 "d2h_bytes_per_step": int(out.nbytes)},
         "gpu_launches": int(gpu_launches),
         "bitops_per_image": 2 * zoo.macs_per_image(spec),
         "achieved_tbitops_network": 2 * zoo.macs_per_image(spec) * value / world / 1e12,
-        "roofline": {"bound": "int-popc", "achieved": achieved, "peak": POPC_PEAK_TBITOPS, "unit": "Tbitop/s",
-                     "frac": achieved / POPC_PEAK_TBITOPS, "traffic": None, "kernel": dom["stage"],
-                     "kernel_share_of_step": dom["ms"] / stage_total, "peak_source": POPC_PEAK_SOURCE},
-        "stages": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in s.items()} for s in stages],
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
+                     "unit": "TOP/s (1 binary MAC = 2 ops = one int8 MAC on +/-1 bytes)",
+                     "frac": achieved / int8_peak, "traffic": traffic, "kernel": dom["stage"],
+                     "kernel_share_of_step": dom["ms"] / stage_total, "peak_source": int8_src,
+                     "popc_pipe_peak": POPC_PEAK_TBITOPS, "popc_peak_source": POPC_PEAK_SOURCE},
+        "stages": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in s_.items()} for s_ in stages],
     }
     return result
+
+
+def stage_traffic(workload, stage_name, index):
+    """DRAM bytes per launch of one stage's kernel from the committed ncu
+    capture (profiles/traffic_<workload>.json, written by
+    tools/ncu_summary.py from `ncu --set full`), or None."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    try:
+        table = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    ent = table.get(str(index))
+    if ent and ent.get("stage") == stage_name:
+        return ent.get("dram_bytes")
+    return None
 
 
 def _dev_stream():
@@ -293,7 +370,8 @@ def stage_macs(st) -> int:
     """Algorithmic binary MACs per image of one device stage."""
     from paper_1705_07175_b200 import network as nw
     if isinstance(st, (nw._Input8Fused, nw._Input8Raw)):
-        return st.units * st.k * 8
+        # tensor cores: one u8 x +/-1 MAC per byte; POPC engine: 8 bit-planes
+        return st.units * st.k * (1 if getattr(st, "tc", False) else 8)
     if isinstance(st, (nw._DenseFused, nw._Dense)):
         return st.rec.units * st.rec.input_len
     if isinstance(st, (nw._ConvFused, nw._Conv, nw._ByteConvFused)):
@@ -304,7 +382,7 @@ def stage_macs(st) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="bcnn", choices=["bcnn", "bmlp"])
     ap.add_argument("--batch", type=int, default=None, help="images per GPU per step")

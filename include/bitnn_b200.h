@@ -221,11 +221,14 @@ int b2_tc_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c
 int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_t* w_i8, int64_t units, b2_thresh th,
                          uint64_t* out, void* stream);
 
-/* _PackedByteBN -> _PackedConv (kh*kw*c <= 128) [-> _Pool 2x2/2] ->
- * _PackedBN, as b2_byte_conv_bn_pack. */
+/* _PackedByteBN -> _PackedConv [-> _Pool 2x2/2] -> _PackedBN, as
+ * b2_byte_conv_bn_pack (c <= 8, kh*kw <= 16, kh*kw*c <= 128).  `codes`
+ * (batch*h*w bytes, caller-provided scratch) receives the byte-batchnorm
+ * bits of every site (the reference's _PackedByteBN output, one byte per
+ * site) before the tensor-core conv gathers them.  Two launches. */
 int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
                             const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
-                            b2_thresh th_out, uint64_t* out, void* stream);
+                            b2_thresh th_out, uint8_t* codes, uint64_t* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -35,6 +35,18 @@ __global__ void k_expand_i8(const uint64_t* __restrict__ w, int64_t rows, int64_
   reinterpret_cast<uint32_t*>(out)[t] = word;
 }
 
+// network.py:128-138 _PackedByteBN on the raw image: one code per site,
+// bit ch = byte batchnorm threshold of channel ch (c <= 8).
+__global__ void k_byte_codes(const uint8_t* __restrict__ x, int64_t sites, int c, const int32_t* __restrict__ t,
+                             const uint8_t* __restrict__ ge, uint8_t* __restrict__ codes) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sites) return;
+  uint32_t code = 0;
+  for (int ch = 0; ch < c; ++ch)
+    code |= (uint32_t)thr_bit((int32_t)x[i * c + ch], __ldg(t + ch), __ldg(ge + ch) != 0) << ch;
+  codes[i] = (uint8_t)code;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -94,8 +106,9 @@ int launch_bn(const Args& g, const int8_t* b_i8, int64_t kpad, cudaStream_t st) 
 // 256-column tiles (one M=128 x N=256 MMA per 32 K: half the A widening and
 // MMA issue per MAC, measured 1.7x faster on 16384^3).
 template <int AM, int EM>
-int launch(const Args& g, const int8_t* b_i8, int64_t kpad, cudaStream_t st) {
+int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k) {
   if (g.M == 0 || g.N == 0) return 0;
+  g.klast = (int)(((k - 1) % BK) / 32 + 1);
   if (g.N <= 128) return launch_bn<128, AM, EM>(g, b_i8, kpad, st);
   return launch_bn<256, AM, EM>(g, b_i8, kpad, st);
 }
@@ -161,7 +174,7 @@ int b2_tc_bgemm(const uint64_t* a, int64_t m, const int8_t* b_i8, int64_t n, int
   g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   g.out_i32 = out;
   g.ldo = n;
-  return tc::launch<tc::A_ROWS, tc::E_I32>(g, b_i8, tc::kpad_of(k), S(stream));
+  return tc::launch<tc::A_ROWS, tc::E_I32>(g, b_i8, tc::kpad_of(k), S(stream), k);
 }
 
 int b2_tc_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl, int32_t k,
@@ -176,7 +189,7 @@ int b2_tc_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, in
   g.N = (int)units;
   g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   tc::pack_args(g, th, out, units);
-  return tc::launch<tc::A_ROWS, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream));
+  return tc::launch<tc::A_ROWS, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 
 int b2_tc_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
@@ -189,7 +202,7 @@ int b2_tc_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c
   g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   g.out_i32 = out;
   g.ldo = filters;
-  return tc::launch<tc::A_CONV, tc::E_I32>(g, w_i8, tc::kpad_of(k), S(stream));
+  return tc::launch<tc::A_CONV, tc::E_I32>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 
 int b2_tc_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
@@ -204,8 +217,8 @@ int b2_tc_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c
   g.N = (int)filters;
   g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   tc::pack_args(g, th, out, filters);
-  if (pool) return tc::launch<tc::A_CONV, tc::E_POOLPACK>(g, w_i8, tc::kpad_of(k), S(stream));
-  return tc::launch<tc::A_CONV, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream));
+  if (pool) return tc::launch<tc::A_CONV, tc::E_POOLPACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
+  return tc::launch<tc::A_CONV, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 
 int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_t* w_i8, int64_t units, b2_thresh th,
@@ -219,25 +232,29 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
   g.N = (int)units;
   g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   tc::pack_args(g, th, out, units);
-  return tc::launch<tc::A_BYTES, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream));
+  return tc::launch<tc::A_BYTES, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 
 int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
                             const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
-                            b2_thresh th_out, uint64_t* out, void* stream) {
-  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > tc::BK ||
-      !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir)
+                            b2_thresh th_out, uint8_t* codes, uint64_t* out, void* stream) {
+  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > tc::BK || c > 8 ||
+      kh * kw > 16 || !codes || !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir)
     return B2_EINVAL;
   tc::Args g{};
-  tc::conv_args(g, x, batch, h, w, c, kh, kw, stride, pad);
+  tc::conv_args(g, codes, batch, h, w, c, kh, kw, stride, pad);
   if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
-  g.in_thresh = th_in.thresh;
-  g.in_ge = th_in.ge_dir;
+  if (!batch) return 0;
+  const int64_t sites = batch * h * w;
+  tc::k_byte_codes<<<(unsigned)cdiv(sites, 256), 256, 0, S(stream)>>>(x, sites, c, th_in.thresh, th_in.ge_dir,
+                                                                      codes);
+  if (int rc = launched()) return rc;
   g.N = (int)filters;
   g.nkb = 1;
+  const int64_t k = (int64_t)kh * kw * c;
   tc::pack_args(g, th_out, out, filters);
-  if (pool) return tc::launch<tc::A_BYTECONV, tc::E_POOLPACK>(g, w_i8, tc::BK, S(stream));
-  return tc::launch<tc::A_BYTECONV, tc::E_PACK>(g, w_i8, tc::BK, S(stream));
+  if (pool) return tc::launch<tc::A_BYTECONV, tc::E_POOLPACK>(g, w_i8, tc::BK, S(stream), k);
+  return tc::launch<tc::A_BYTECONV, tc::E_PACK>(g, w_i8, tc::BK, S(stream), k);
 }
 
 }  // extern "C"

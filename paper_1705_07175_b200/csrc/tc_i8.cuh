@@ -64,7 +64,8 @@ struct Args {
   // ---- problem
   int64_t M;
   int N;
-  int nkb;  // K blocks of 128
+  int nkb;    // K blocks of 128
+  int klast;  // K=32 MMAs carrying data in the last block (1..4)
   // ---- epilogue
   int32_t* out_i32;
   int64_t ldo;
@@ -312,22 +313,38 @@ struct ACursor {
         x = __ldg(reinterpret_cast<const uint2*>(base + ((int64_t)iy * g.W + ix) * g.sstride + within));
       }
     } else if constexpr (AM == A_BYTECONV) {
-      // byte batchnorm (network.py:128-138) of the window's bytes, K order
-      // (dy, dx, c) with c fastest (layers.py:3-8); padding cells invalid
+      // window of byte-batchnorm site codes (c <= 8 bits per site, written by
+      // k_byte_codes = network.py:128-138 _PackedByteBN), K order (dy, dx, c)
+      // with c fastest (layers.py:3-8); padding cells are invalid (byte 0)
       if (mok && kb == 0) {
-        const int kbits = g.kh * g.kw * g.c;
-        const int lo = 64 * half, hi = kbits < lo + 64 ? kbits : lo + 64;
-        const uint8_t* xi = reinterpret_cast<const uint8_t*>(g.a) + img * (int64_t)g.H * g.W * g.c;
-        uint64_t bits = 0, valid = 0;
-        for (int p = lo; p < hi; ++p) {
-          const int cellp = p / g.c, ch = p - cellp * g.c;
-          const int iy = iy0 + cellp / g.kw, ix = ix0 + cellp % g.kw;
-          if (iy < 0 || iy >= g.H || ix < 0 || ix >= g.W) continue;
-          const int32_t v = __ldg(xi + ((int64_t)iy * g.W + ix) * g.c + ch);
-          const bool b = thr_bit(v, __ldg(g.in_thresh + ch), __ldg(g.in_ge + ch) != 0);
-          bits |= (uint64_t)b << (p - lo);
-          valid |= 1ull << (p - lo);
+        const uint8_t* codes = reinterpret_cast<const uint8_t*>(g.a) + img * (int64_t)g.H * g.W;
+        const int ncell = g.kh * g.kw;
+        const uint32_t cmask = (1u << g.c) - 1u;
+        uint64_t b0 = 0, b1 = 0, v0 = 0, v1 = 0;
+        uint32_t code[16];
+        bool cok[16];
+        int dy = 0, dx = 0;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {  // all loads first: one latency per row
+          const int iy = iy0 + dy, ix = ix0 + dx;
+          cok[cc] = cc < ncell && iy >= 0 && iy < g.H && ix >= 0 && ix < g.W;
+          code[cc] = cok[cc] ? __ldg(codes + (int64_t)iy * g.W + ix) : 0u;
+          if (++dx == g.kw) dx = 0, ++dy;
         }
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          const int pos = cc * g.c;
+          const uint64_t cb = code[cc], vb = cok[cc] ? cmask : 0u;
+          if (pos < 64) {
+            b0 |= cb << pos;
+            v0 |= vb << pos;
+            if (pos + g.c > 64) b1 |= cb >> (64 - pos), v1 |= vb >> (64 - pos);
+          } else if (pos < 128) {
+            b1 |= cb << (pos - 64);
+            v1 |= vb << (pos - 64);
+          }
+        }
+        const uint64_t bits = half ? b1 : b0, valid = half ? v1 : v0;
         x = make_uint2((uint32_t)bits, (uint32_t)(bits >> 32));
         vm = make_uint2((uint32_t)valid, (uint32_t)(valid >> 32));
       }
@@ -361,6 +378,31 @@ constexpr int stages() {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+constexpr int THR_COLS = 2048;  // resident threshold table (columns)
+
+// Threshold table for columns [n0, n0 + ncols) (ncols % 128 == 0), built by
+// the 128 epilogue threads: ge -> (1, -t), le -> (-1, t), column beyond N ->
+// (0, -1) = bit 0; one ge-direction mask word per 32 columns (ballot).
+__device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncols, int r, int lane, int4* sthr,
+                                                 uint32_t* sgm) {
+  int* st = reinterpret_cast<int*>(sthr);
+  for (int j = r; j < ncols; j += 128) {
+    const int n = n0 + j;
+    int mul = 0, add = -1;
+    bool ge = true;
+    if (n < g.N) {
+      const int32_t th = __ldg(g.thresh + n);
+      ge = __ldg(g.ge + n) != 0;
+      mul = ge ? 1 : -1;
+      add = ge ? -th : th;
+    }
+    st[2 * j] = mul;
+    st[2 * j + 1] = add;
+    const uint32_t gmw = __ballot_sync(0xffffffffu, ge);
+    if (lane == 0) sgm[j >> 5] = gmw;
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 template <int BN, int AM, int EM>
 __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap, const Args g) {
@@ -376,9 +418,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sb = smem;                                                      // STAGES x B_STAGE_BYTES
-  int4* sthr = reinterpret_cast<int4*>(smem + STAGES * B_STAGE_BYTES);     // BN/2 x (mul, add, mul, add)
-  uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + BN / 2);              // BN/32 ge-direction masks
-  uint64_t* full = reinterpret_cast<uint64_t*>(sgm + 8);
+  int4* sthr = reinterpret_cast<int4*>(smem + STAGES * B_STAGE_BYTES);     // THR_COLS/2 x (mul, add, mul, add)
+  uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + THR_COLS / 2);        // THR_COLS/32 ge-direction masks
+  uint64_t* full = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -441,9 +483,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           tc_fence_after();
           const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
           const uint32_t bs = smem_u32(sb + s * B_STAGE_BYTES);
+          const int kmma = kb + 1 == g.nkb ? g.klast : BK / 32;
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k)
-            tc_mma_i8(d, a + k * 8, sw128_desc(bs + k * 32), IDESC, (kb | k) ? 1u : 0u);
+            if (k < kmma) tc_mma_i8(d, a + k * 8, sw128_desc(bs + k * 32), IDESC, (kb | k) ? 1u : 0u);
           tc_commit(&empty[s]);
           if (++s == STAGES) s = 0, ph ^= 1;
         }
@@ -552,36 +595,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int acc = 0;
     uint32_t aph = 0;
+    // thresholds as bit = (acc * mul + add >= 0), resident for the launch
+    // when all N columns fit the table, else staged per tile
+    const int ncols = ntiles * BN;
+    const bool static_thr = ncols <= THR_COLS;
+    if constexpr (EM != E_I32) {
+      if (static_thr) {
+        stage_thresholds(g, 0, ncols, r, lane, sthr, sgm);
+        epi_bar();
+      }
+    }
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int64_t m = (t % mtiles) * BM + r;
       const int n0 = (int)(t / mtiles) * BN;
+      const int tcol = static_thr ? n0 : 0;  // table column of this tile's first column
       const bool mok = m < g.M;
       if constexpr (EM != E_I32) {
-        // this tile's thresholds as bit = (acc * mul + add >= 0):
-        // ge -> (1, -t), le -> (-1, t), column beyond N -> (0, -1) = bit 0
-        epi_bar();
-        int* st = reinterpret_cast<int*>(sthr);
-        for (int j = r; j < BN; j += 128) {
-          const int n = n0 + j;
-          int mul = 0, add = -1;
-          if (n < g.N) {
-            const int32_t th = __ldg(g.thresh + n);
-            const bool ge = __ldg(g.ge + n) != 0;
-            mul = ge ? 1 : -1;
-            add = ge ? -th : th;
-          }
-          st[2 * j] = mul;
-          st[2 * j + 1] = add;
+        if (!static_thr) {  // N too wide for the resident table: this tile's columns only
+          epi_bar();
+          stage_thresholds(g, n0, BN, r, lane, sthr, sgm);
+          epi_bar();
         }
-        if (r < BN / 32) {
-          uint32_t gmw = 0;
-          for (int j = 0; j < 32; ++j) {
-            const int n = n0 + 32 * r + j;
-            gmw |= (uint32_t)(n >= g.N || __ldg(g.ge + n) != 0) << j;
-          }
-          sgm[r] = gmw;
-        }
-        epi_bar();
       }
       mbar_wait_sleep(&tfull[acc], aph, 256);
       tc_fence_after();
@@ -610,7 +644,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           uint32_t sg = 0;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const int4 p = sthr[c * 16 + j / 2];
+            const int4 p = sthr[(tcol + c * 32 + j) / 2];
             const int d0 = (int)v[j] * p.x + p.y;
             const int d1 = (int)v[j + 1] * p.z + p.w;
             sg = __funnelshift_l((uint32_t)d0, sg, 1);
@@ -620,7 +654,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           if constexpr (EM == E_POOLPACK) {
             // max over the 2x2 window then threshold == OR (ge) / AND (le)
             // of the four thresholded rows (monotone threshold)
-            const uint32_t gm = sgm[c];
+            const uint32_t gm = sgm[(tcol >> 5) + c];
             uint32_t o = w | __shfl_xor_sync(0xffffffffu, w, 1);
             o |= __shfl_xor_sync(0xffffffffu, o, 2);
             uint32_t a = w & __shfl_xor_sync(0xffffffffu, w, 1);
@@ -663,7 +697,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
 
 template <int BN>
 constexpr int smem_bytes() {
-  return stages<BN>() * BN * BK + BN * 8 + 32 + 8 * (2 * stages<BN>() + 4) + 16 + 1024;
+  return stages<BN>() * BN * BK + THR_COLS * 8 + THR_COLS / 8 + 8 * (2 * stages<BN>() + 4) + 16 + 1024;
 }
 
 }  // namespace tc

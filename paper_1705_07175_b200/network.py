@@ -136,13 +136,21 @@ class _ByteConvFused(_Stage):
         self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
         self.w = _dev.upload(rec.words)
         self.bn0, self.bn1 = bn0, bn1
-        self.tc = _lib.ENGINE == "tc" and rec.k <= 128
+        self.tc = _lib.ENGINE == "tc" and rec.k <= 128 and c <= 8 and rec.kh * rec.kw <= 16
         if not self.tc and (rec.k > 32 or rec.filters > 1024):
             raise AssertionError("planner chose the fused byte conv for an ineligible shape")
         self.w8 = _dev.widen_i8(self.w, rec.filters, rec.k) if self.tc else None
 
     def per_image(self):
         return (self.h_out * self.w_out, _wpl(self.rec.filters))
+
+    def alloc(self, cap):
+        super().alloc(cap)
+        h, w, c = self.in_shape
+        self.codes = _dev.empty((cap * h * w,), np.uint8) if self.tc else None
+
+    def launches(self):
+        return 2 if self.tc else 1
 
     def launch(self, net, batch, st):
         h, w, c = self.in_shape
@@ -151,7 +159,8 @@ class _ByteConvFused(_Stage):
             _lib.call("b2_tc_byte_conv_bn_pack", self.src_ptr(net), batch, h, w, c,
                       _thresh_struct(self.bn0["thresh32"], self.bn0["thresh64"], self.bn0["ge"]), _dev.P(self.w8),
                       r.filters, r.kh, r.kw, r.stride, r.pad, 0,
-                      _thresh_struct(self.bn1["thresh32"], self.bn1["thresh64"], self.bn1["ge"]), _dev.P(self.out), st)
+                      _thresh_struct(self.bn1["thresh32"], self.bn1["thresh64"], self.bn1["ge"]), _dev.P(self.codes),
+                      _dev.P(self.out), st)
             return
         _lib.call("b2_byte_conv_bn_pack", self.src_ptr(net), batch, h, w, c,
                   _thresh_struct(self.bn0["thresh32"], self.bn0["thresh64"], self.bn0["ge"]), _dev.P(self.w),
@@ -518,7 +527,10 @@ class Network:
             elif kind == "bytebn":
                 h, w, c = op["dims"]
                 conv = nxt if nxt is not None and nxt["kind"] == "conv" else None
-                kmax, fmax = (128, 1 << 30) if _lib.ENGINE == "tc" else (32, 1024)
+                crec = conv["rec"] if conv is not None else None
+                tc_ok = (_lib.ENGINE == "tc" and crec is not None and crec.k <= 128 and c <= 8
+                         and crec.kh * crec.kw <= 16)
+                kmax, fmax = (128, 1 << 30) if tc_ok else (32, 1024)
                 if (conv is not None and not op["flat"] and conv["rec"].k <= kmax and 1 < conv["rec"].filters <= fmax
                         and nxt2 is not None and nxt2["kind"] == "bn"
                         and (not nxt2["flat"] or conv["rec"].filters % 64 == 0)):

@@ -1,0 +1,45 @@
+"""Launch one stage of a baseline network eagerly (for ncu captures).
+
+    python tools/profile_stage.py --workload bcnn --stage 0 --batch 8192 --reps 3
+
+The network is built and warmed once; then stage `--stage` is launched
+`--reps` times on the current stream.  Use with
+`ncu -k regex:k_tc_gemm -s <skip> -c 1 ...`."""
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1705_07175_b200 import _dev, zoo  # noqa: E402
+from paper_1705_07175_b200.network import Network  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="bcnn", choices=["bcnn", "bmlp"])
+    ap.add_argument("--stage", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=8192)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    spec = zoo.bcnn_spec() if a.workload == "bcnn" else zoo.bmlp_spec()
+    net = Network(spec, max_batch=a.batch, use_graphs=False)
+    rng = np.random.default_rng(0)
+    n = net.input_len
+    net.input_device.copy_(torch.from_numpy(rng.integers(0, 256, (a.batch, n), dtype=np.uint8)).cuda())
+    net.run(a.batch)
+    torch.cuda.synchronize()
+    st = net.stages[a.stage]
+    for _ in range(a.reps):
+        st.launch(net, a.batch, _dev.stream())
+    torch.cuda.synchronize()
+    print("stage", a.stage, st.name, "launches/stage", st.launches())
+
+
+if __name__ == "__main__":
+    main()
