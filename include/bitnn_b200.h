@@ -222,13 +222,14 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
                          uint64_t* out, void* stream);
 
 /* _PackedByteBN -> _PackedConv [-> _Pool 2x2/2] -> _PackedBN, as
- * b2_byte_conv_bn_pack (c <= 8, kh*kw <= 16, kh*kw*c <= 128).  `codes`
- * (batch*h*w bytes, caller-provided scratch) receives the byte-batchnorm
- * bits of every site (the reference's _PackedByteBN output, one byte per
- * site) before the tensor-core conv gathers them.  Two launches. */
+ * b2_byte_conv_bn_pack (kh*kw*c <= 128).  Two launches: the byte batchnorm
+ * + bit im2col (_kernels.py:170-199) of every output pixel into `scratch`
+ * (b2_tc_byte_conv_scratch_bytes bytes: window bits plus a validity mask,
+ * padding cells invalid), then the tensor-core GEMM with zero padding. */
+int64_t b2_tc_byte_conv_scratch_bytes(int64_t batch, int h, int w, int c, int kh, int kw, int stride, int pad);
 int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
                             const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
-                            b2_thresh th_out, uint8_t* codes, uint64_t* out, void* stream);
+                            b2_thresh th_out, void* scratch, uint64_t* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,7 @@ SIGNATURES = {
     "b2_tc_conv_forward": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, vp, vp]),
     "b2_tc_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, cint, Thresh, vp, vp]),
     "b2_tc_input8_bn_pack": (cint, [vp, i64, i64, vp, i64, Thresh, vp, vp]),
+    "b2_tc_byte_conv_scratch_bytes": (i64, [i64, cint, cint, cint, cint, cint, cint, cint]),
     "b2_tc_byte_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, Thresh, vp, i64, cint, cint, cint, cint, cint,
                                        Thresh, vp, vp, vp]),
 }

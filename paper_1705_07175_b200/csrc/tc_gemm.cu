@@ -35,16 +35,51 @@ __global__ void k_expand_i8(const uint64_t* __restrict__ w, int64_t rows, int64_
   reinterpret_cast<uint32_t*>(out)[t] = word;
 }
 
-// network.py:128-138 _PackedByteBN on the raw image: one code per site,
-// bit ch = byte batchnorm threshold of channel ch (c <= 8).
-__global__ void k_byte_codes(const uint8_t* __restrict__ x, int64_t sites, int c, const int32_t* __restrict__ t,
-                             const uint8_t* __restrict__ ge, uint8_t* __restrict__ codes) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= sites) return;
-  uint32_t code = 0;
-  for (int ch = 0; ch < c; ++ch)
-    code |= (uint32_t)thr_bit((int32_t)x[i * c + ch], __ldg(t + ch), __ldg(ge + ch) != 0) << ch;
-  codes[i] = (uint8_t)code;
+// network.py:128-138 _PackedByteBN on the raw image followed by the bit
+// im2col of _kernels.py:170-199 (unroll_packed), one thread per output
+// pixel: row = kw32 words of window bits (K order (dy, dx, c), c fastest)
+// then kw32 words of validity (0 for window cells in the padding ring, so
+// the tensor cores see zero padding and no correction map is needed).
+__global__ void k_byte_unroll(const uint8_t* __restrict__ x, int64_t rows, int h, int w, int c, int kh, int kw,
+                              int stride, int pad, int ho, int wo, int kw32, int pooled,
+                              const int32_t* __restrict__ t, const uint8_t* __restrict__ ge,
+                              uint32_t* __restrict__ out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t hw = (int64_t)ho * wo;
+  const int64_t img = r / hw;
+  const int pos = (int)(r - img * hw);
+  int oy, ox;
+  if (pooled) {  // pool-window-major rows, as tc::row_pos<true>
+    const int q = pos >> 2, cell = pos & 3, wp = wo >> 1;
+    oy = 2 * (q / wp) + (cell >> 1);
+    ox = 2 * (q % wp) + (cell & 1);
+  } else {
+    oy = pos / wo;
+    ox = pos - oy * wo;
+  }
+  const uint8_t* xi = x + img * (int64_t)h * w * c;
+  uint32_t bits[4] = {0, 0, 0, 0}, valid[4] = {0, 0, 0, 0};
+  int p = 0;
+  for (int dy = 0; dy < kh; ++dy) {
+    const int iy = oy * stride + dy - pad;
+    for (int dx = 0; dx < kw; ++dx) {
+      const int ix = ox * stride + dx - pad;
+      const bool ok = iy >= 0 && iy < h && ix >= 0 && ix < w;
+      const uint8_t* px = xi + ((int64_t)iy * w + ix) * c;
+      for (int ch = 0; ch < c; ++ch, ++p) {
+        if (!ok) continue;
+        const bool b = thr_bit((int32_t)__ldg(px + ch), __ldg(t + ch), __ldg(ge + ch) != 0);
+        bits[p >> 5] |= (uint32_t)b << (p & 31);
+        valid[p >> 5] |= 1u << (p & 31);
+      }
+    }
+  }
+  uint32_t* o = out + r * 2 * kw32;
+  for (int i = 0; i < kw32; ++i) {
+    o[i] = bits[i];
+    o[kw32 + i] = valid[i];
+  }
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -93,12 +128,12 @@ int launch_bn(const Args& g, const int8_t* b_i8, int64_t kpad, cudaStream_t st) 
   auto kern = k_tc_gemm<BN, AM, EM>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<BN>());
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<BN, AM>());
     attr = true;
   }
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, NUM_THREADS, smem_bytes<BN>(), st>>>(map, g);
+  kern<<<grid, NUM_THREADS, smem_bytes<BN, AM>(), st>>>(map, g);
   return launched();
 }
 
@@ -235,23 +270,35 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
   return tc::launch<tc::A_BYTES, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 
+int64_t b2_tc_byte_conv_scratch_bytes(int64_t batch, int h, int w, int c, int kh, int kw, int stride, int pad) {
+  if (!tc::conv_ok(batch, h, w, c, 1, kh, kw, stride, pad)) return -1;
+  const int64_t ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  const int64_t kw32 = ((int64_t)kh * kw * c + 31) / 32;
+  return batch * ho * wo * 2 * kw32 * 4;
+}
+
 int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
                             const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
-                            b2_thresh th_out, uint8_t* codes, uint64_t* out, void* stream) {
-  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > tc::BK || c > 8 ||
-      kh * kw > 16 || !codes || !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir)
+                            b2_thresh th_out, void* scratch, uint64_t* out, void* stream) {
+  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > tc::BK || !scratch ||
+      !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir)
     return B2_EINVAL;
   tc::Args g{};
-  tc::conv_args(g, codes, batch, h, w, c, kh, kw, stride, pad);
+  tc::conv_args(g, x, batch, h, w, c, kh, kw, stride, pad);
   if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
   if (!batch) return 0;
-  const int64_t sites = batch * h * w;
-  tc::k_byte_codes<<<(unsigned)cdiv(sites, 256), 256, 0, S(stream)>>>(x, sites, c, th_in.thresh, th_in.ge_dir,
-                                                                      codes);
+  const int64_t k = (int64_t)kh * kw * c;
+  const int kw32 = (int)((k + 31) / 32);
+  tc::k_byte_unroll<<<(unsigned)cdiv(g.M, 256), 256, 0, S(stream)>>>(x, g.M, h, w, c, kh, kw, stride, pad, g.Ho,
+                                                                     g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
+                                                                     reinterpret_cast<uint32_t*>(scratch));
   if (int rc = launched()) return rc;
+  // rows are ordered like the conv output (pool-window-major when pooled)
+  g.a = reinterpret_cast<const uint32_t*>(scratch);
+  g.lda = 2 * kw32;
+  g.awords = kw32;
   g.N = (int)filters;
   g.nkb = 1;
-  const int64_t k = (int64_t)kh * kw * c;
   tc::pack_args(g, th_out, out, filters);
   if (pool) return tc::launch<tc::A_BYTECONV, tc::E_POOLPACK>(g, w_i8, tc::BK, S(stream), k);
   return tc::launch<tc::A_BYTECONV, tc::E_PACK>(g, w_i8, tc::BK, S(stream), k);

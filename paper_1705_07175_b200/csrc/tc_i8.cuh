@@ -44,11 +44,12 @@ namespace tc {
 
 constexpr int BM = 128;                 // tile rows = TMEM lanes
 constexpr int BK = 128;                 // int8 K per stage = one 128-byte swizzle atom
-constexpr int STAGES_MAX = 8;           // smem B ring and TMEM A ring depth (BN <= 128)
 constexpr int A_STAGE_COLS = BK / 4;    // 32 TMEM columns per A stage
 constexpr int NUM_THREADS = 512;
 constexpr int PF = 4;                   // A-producer prefetch depth (K blocks)
 
+// A operand sources: packed rows; implicit bit-im2col of NHWC-bits
+// activations; raw u8 rows; masked window rows of the byte-input first conv
 enum AMode { A_ROWS = 0, A_CONV = 1, A_BYTES = 2, A_BYTECONV = 3 };
 enum EMode { E_I32 = 0, E_PACK = 1, E_POOLPACK = 2 };
 
@@ -56,11 +57,9 @@ struct Args {
   // ---- A operand
   const uint32_t* a;  // packed rows / NHWC-bits activations / bytes (as words)
   int64_t lda;        // A_ROWS/A_BYTES: uint32 words per row
-  int awords;         // A_ROWS: valid uint32 words per row (ceil(K/32)); A_BYTES: valid bytes per row (K)
+  int awords;         // A_ROWS/A_BYTECONV: valid uint32 words per row (ceil(K/32)); A_BYTES: valid words
   // conv geometry (A_CONV: spw = C/32 words per site; A_BYTECONV: c = channels)
   int H, W, spw, sstride, kh, kw, stride, pad, Ho, Wo, c;
-  const int32_t* in_thresh;  // A_BYTECONV: byte batchnorm thresholds (per channel)
-  const uint8_t* in_ge;
   // ---- problem
   int64_t M;
   int N;
@@ -253,18 +252,16 @@ struct ACursor {
     kb = 0;
     const int64_t m = (t % mtiles) * BM + r;
     mok = t < tiles && m < g.M;
-    if constexpr (AM == A_CONV || AM == A_BYTECONV) {
+    if constexpr (AM == A_CONV) {
       img = 0;
       int oy = 0, ox = 0;
       if (mok) row_pos<POOLED>(g, m, img, oy, ox);
       iy0 = oy * g.stride - g.pad;
       ix0 = ox * g.stride - g.pad;
-      if constexpr (AM == A_CONV) {
-        base = g.a + img * (int64_t)g.H * g.W * g.sstride;
-        cell = dy = dx = 0;
-        within = 2 * half;
-        while (within >= g.spw) within -= g.spw, step_cell(g);
-      }
+      base = g.a + img * (int64_t)g.H * g.W * g.sstride;
+      cell = dy = dx = 0;
+      within = 2 * half;
+      while (within >= g.spw) within -= g.spw, step_cell(g);
     } else {
       base = g.a + (mok ? m : 0) * g.lda;
     }
@@ -313,40 +310,13 @@ struct ACursor {
         x = __ldg(reinterpret_cast<const uint2*>(base + ((int64_t)iy * g.W + ix) * g.sstride + within));
       }
     } else if constexpr (AM == A_BYTECONV) {
-      // window of byte-batchnorm site codes (c <= 8 bits per site, written by
-      // k_byte_codes = network.py:128-138 _PackedByteBN), K order (dy, dx, c)
-      // with c fastest (layers.py:3-8); padding cells are invalid (byte 0)
-      if (mok && kb == 0) {
-        const uint8_t* codes = reinterpret_cast<const uint8_t*>(g.a) + img * (int64_t)g.H * g.W;
-        const int ncell = g.kh * g.kw;
-        const uint32_t cmask = (1u << g.c) - 1u;
-        uint64_t b0 = 0, b1 = 0, v0 = 0, v1 = 0;
-        uint32_t code[16];
-        bool cok[16];
-        int dy = 0, dx = 0;
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {  // all loads first: one latency per row
-          const int iy = iy0 + dy, ix = ix0 + dx;
-          cok[cc] = cc < ncell && iy >= 0 && iy < g.H && ix >= 0 && ix < g.W;
-          code[cc] = cok[cc] ? __ldg(codes + (int64_t)iy * g.W + ix) : 0u;
-          if (++dx == g.kw) dx = 0, ++dy;
-        }
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-          const int pos = cc * g.c;
-          const uint64_t cb = code[cc], vb = cok[cc] ? cmask : 0u;
-          if (pos < 64) {
-            b0 |= cb << pos;
-            v0 |= vb << pos;
-            if (pos + g.c > 64) b1 |= cb >> (64 - pos), v1 |= vb >> (64 - pos);
-          } else if (pos < 128) {
-            b1 |= cb << (pos - 64);
-            v1 |= vb << (pos - 64);
-          }
-        }
-        const uint64_t bits = half ? b1 : b0, valid = half ? v1 : v0;
-        x = make_uint2((uint32_t)bits, (uint32_t)(bits >> 32));
-        vm = make_uint2((uint32_t)valid, (uint32_t)(valid >> 32));
+      // masked rows written by k_byte_unroll: awords bit words then awords
+      // validity words per row (padding cells of the window -> byte 0)
+      const int w0 = kb * 4 + 2 * half;
+      if (mok) {
+        const uint32_t* p = base + w0;
+        if (w0 + 0 < g.awords) x.x = __ldg(p + 0), vm.x = __ldg(p + g.awords + 0);
+        if (w0 + 1 < g.awords) x.y = __ldg(p + 1), vm.y = __ldg(p + g.awords + 1);
       }
     }
   }
@@ -371,9 +341,24 @@ struct ACursor {
   }
 };
 
-template <int BN>
-constexpr int stages() {
-  return BN <= 128 ? STAGES_MAX : 6;  // 6 x 32 KB B stages at BN = 256
+// Pipeline shape per (BN, A mode).  Two independent rings: the shared-memory
+// B ring (TMA) and the TMEM A ring (producers); the MMA waits on both.
+// TMEM holds ACC_BUFS accumulators of BN columns plus A_STAGES A stages of
+// 32 columns (512 columns in all).  The B ring is as deep as shared memory
+// allows (192 KB) so TMA runs >= 3 us ahead of the tensor cores.  The
+// first conv has one K block per tile, so its accumulator ring is deeper
+// (3 x 128) to hide the MMA -> epilogue hand-off, with a 4-stage A ring.
+template <int BN, int AM = A_ROWS>
+constexpr int a_stages() {
+  return AM == A_BYTECONV ? 4 : 8;
+}
+template <int BN, int AM = A_ROWS>
+constexpr int b_stages() {
+  return (192 * 1024) / (BN * BK);  // 12 x 16 KB at BN = 128, 6 x 32 KB at BN = 256
+}
+template <int BN, int AM = A_ROWS>
+constexpr int acc_bufs() {
+  return BN > 128 ? 1 : (AM == A_BYTECONV ? 3 : 2);
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -408,23 +393,28 @@ template <int BN, int AM, int EM>
 __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap, const Args g) {
   constexpr bool POOLED = (EM == E_POOLPACK);
   constexpr int B_STAGE_BYTES = BN * BK;
-  constexpr int STAGES = stages<BN>();
+  constexpr int SA = a_stages<BN, AM>();
+  constexpr int SB = b_stages<BN, AM>();
   constexpr int ACC_COLS = BN;
-  constexpr int ACC_BUFS = BN <= 128 ? 2 : 1;  // accumulator double buffer when TMEM allows
+  constexpr int ACC_BUFS = acc_bufs<BN, AM>();
   constexpr int A_COL0 = ACC_BUFS * ACC_COLS;
-  static_assert(A_COL0 + STAGES * A_STAGE_COLS <= 512, "TMEM budget");
+  static_assert(A_COL0 + SA * A_STAGE_COLS <= 512, "TMEM budget");
   constexpr uint32_t IDESC = idesc_i8(BN, AM == A_BYTES);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sb = smem;                                                      // STAGES x B_STAGE_BYTES
-  int4* sthr = reinterpret_cast<int4*>(smem + STAGES * B_STAGE_BYTES);     // THR_COLS/2 x (mul, add, mul, add)
+  // 1024-byte alignment by pointer arithmetic on the shared array (an
+  // integer round trip would turn every table read into a generic load)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sb = smem;                                                      // SB x B_STAGE_BYTES
+  int4* sthr = reinterpret_cast<int4*>(smem + SB * B_STAGE_BYTES);         // THR_COLS/2 x (mul, add, mul, add)
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + THR_COLS / 2);        // THR_COLS/32 ge-direction masks
-  uint64_t* full = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
+  uint64_t* bempty = bfull + SB;
+  uint64_t* full = bempty + SB;  // A ring
+  uint64_t* empty = full + SA;
+  uint64_t* tfull = empty + SA;
+  uint64_t* tempty = tfull + ACC_BUFS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC_BUFS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mtiles = (g.M + BM - 1) / BM;
@@ -432,11 +422,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   const int64_t tiles = mtiles * ntiles;  // tile t -> (m tile t % mtiles, n tile t / mtiles)
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 8 + 1);  // 8 A-producer warps + the TMA expect_tx arrival
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&bfull[s], 1);  // the TMA expect_tx arrival
+      mbar_init(&bempty[s], 1);
+    }
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&full[s], 8);  // 8 A-producer warps
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < ACC_BUFS; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
@@ -460,18 +454,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int n0 = (int)(t / mtiles) * BN;
         for (int kb = 0; kb < g.nkb; ++kb) {
-          mbar_wait_sleep(&empty[s], ph ^ 1, 64);
-          mbar_expect_tx(&full[s], B_STAGE_BYTES);
-          tma_load_2d(sb + s * B_STAGE_BYTES, &bmap, &full[s], kb * BK, n0);
-          if (++s == STAGES) s = 0, ph ^= 1;
+          mbar_wait(&bempty[s], ph ^ 1);
+          mbar_expect_tx(&bfull[s], B_STAGE_BYTES);
+          tma_load_2d(sb + s * B_STAGE_BYTES, &bmap, &bfull[s], kb * BK, n0);
+          if (++s == SB) s = 0, ph ^= 1;
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
+      int s = 0, sb_ = 0;
+      uint32_t ph = 0, bph = 0;
       int acc = 0;
       uint32_t aph = 0;
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -479,16 +473,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
         for (int kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait(&bfull[sb_], bph);
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
-          const uint32_t bs = smem_u32(sb + s * B_STAGE_BYTES);
+          const uint32_t bs = smem_u32(sb + sb_ * B_STAGE_BYTES);
           const int kmma = kb + 1 == g.nkb ? g.klast : BK / 32;
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k)
             if (k < kmma) tc_mma_i8(d, a + k * 8, sw128_desc(bs + k * 32), IDESC, (kb | k) ? 1u : 0u);
+          tc_commit(&bempty[sb_]);
           tc_commit(&empty[s]);
-          if (++s == STAGES) s = 0, ph ^= 1;
+          if (++s == SA) s = 0, ph ^= 1;
+          if (++sb_ == SB) sb_ = 0, bph ^= 1;
         }
         tc_commit(&tfull[acc]);
         if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
@@ -547,37 +544,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
             cur.fetch_bytes(g, half, qx[u]);
             cur.advance(g, gridDim.x, mtiles, tiles, r, half);
             publish(s, v);
-            if (++s == STAGES) s = 0, ph ^= 1;
+            if (++s == SA) s = 0, ph ^= 1;
           }
         }
       }
     } else {
-      uint2 qx[PF], qv[PF];
+      // BYTECONV keeps a per-bit validity word per slot; the row and conv
+      // modes only a flag (valid rows widen to +/-1, invalid ones to 0)
+      constexpr bool MASKED = AM == A_BYTECONV;
+      uint2 qx[PF], qv[MASKED ? PF : 1];
+      bool qok[PF];
 #pragma unroll
       for (int u = 0; u < PF; ++u) {
-        cur.fetch_bits(g, half, qx[u], qv[u]);
+        uint2 vm;
+        cur.fetch_bits(g, half, qx[u], vm);
+        if constexpr (MASKED) qv[u] = vm;
+        qok[u] = vm.x != 0 || vm.y != 0;
         cur.advance(g, gridDim.x, mtiles, tiles, r, half);
       }
-      for (int64_t j0 = 0; j0 < jobs; j0 += PF) {
+      const int ijobs = (int)jobs;
+      for (int j0 = 0; j0 < ijobs; j0 += PF) {
 #pragma unroll
         for (int u = 0; u < PF; ++u) {
-          if (j0 + u < jobs) {
+          if (j0 + u < ijobs) {
             uint32_t v[16];
 #ifndef B2_PROBE_SKIP_A
-            if constexpr (AM == A_BYTECONV) {
+            if constexpr (MASKED) {
               widen32m(qx[u].x, qv[u].x, v + 0);
               widen32m(qx[u].y, qv[u].y, v + 8);
             } else {
-              widen32(qx[u].x, qv[u].x != 0, v + 0);
-              widen32(qx[u].y, qv[u].y != 0, v + 8);
+              widen32(qx[u].x, qok[u], v + 0);
+              widen32(qx[u].y, qok[u], v + 8);
             }
 #endif
             // refill the slot only after it was consumed: the load lands in
             // the same registers and nothing waits on it until PF stages later
-            cur.fetch_bits(g, half, qx[u], qv[u]);
+            uint2 vm;
+            cur.fetch_bits(g, half, qx[u], vm);
+            if constexpr (MASKED) qv[u] = vm;
+            qok[u] = vm.x != 0 || vm.y != 0;
             cur.advance(g, gridDim.x, mtiles, tiles, r, half);
             publish(s, v);
-            if (++s == STAGES) s = 0, ph ^= 1;
+            if (++s == SA) s = 0, ph ^= 1;
           }
         }
       }
@@ -617,14 +625,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           epi_bar();
         }
       }
-      mbar_wait_sleep(&tfull[acc], aph, 256);
+#ifdef B2_EPI_SLEEP
+      mbar_wait_sleep(&tfull[acc], aph, B2_EPI_SLEEP);
+#else
+      mbar_wait(&tfull[acc], aph);
+#endif
       tc_fence_after();
       uint32_t words[BN / 32];
+      const int4* trow = sthr + (tcol >> 1);  // (mul, add) pairs of this tile's columns
+      // TMEM -> registers, software-pipelined: chunk c + 1 is in flight while
+      // chunk c is thresholded (tcgen05.wait::ld waits for all prior loads)
+      uint32_t va[32], vb[32];
+      tmem_ld32(tmem + lane_addr + acc * ACC_COLS, va);
+      tmem_wait_ld();
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem + lane_addr + acc * ACC_COLS + c * 32, v);
-        tmem_wait_ld();
+        uint32_t(&v)[32] = (c & 1) ? vb : va;
+        uint32_t(&vn)[32] = (c & 1) ? va : vb;
+        if (c + 1 < BN / 32) tmem_ld32(tmem + lane_addr + acc * ACC_COLS + (c + 1) * 32, vn);
         const int nb = n0 + c * 32;
         if constexpr (EM == E_I32) {
           if (mok && nb < g.N) {
@@ -644,7 +662,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           uint32_t sg = 0;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const int4 p = sthr[(tcol + c * 32 + j) / 2];
+            const int4 p = trow[c * 16 + j / 2];
             const int d0 = (int)v[j] * p.x + p.y;
             const int d1 = (int)v[j + 1] * p.z + p.w;
             sg = __funnelshift_l((uint32_t)d0, sg, 1);
@@ -663,6 +681,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           }
           words[c] = w;
         }
+        if (c + 1 < BN / 32) tmem_wait_ld();
       }
       tc_fence_before();
       __syncwarp();
@@ -695,9 +714,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   }
 }
 
-template <int BN>
+template <int BN, int AM>
 constexpr int smem_bytes() {
-  return stages<BN>() * BN * BK + THR_COLS * 8 + THR_COLS / 8 + 8 * (2 * stages<BN>() + 4) + 16 + 1024;
+  return b_stages<BN, AM>() * BN * BK + THR_COLS * 8 + THR_COLS / 8 +
+         8 * (2 * b_stages<BN, AM>() + 2 * a_stages<BN, AM>() + 6) + 16 + 1024;
 }
 
 }  // namespace tc

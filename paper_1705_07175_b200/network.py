@@ -136,7 +136,7 @@ class _ByteConvFused(_Stage):
         self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
         self.w = _dev.upload(rec.words)
         self.bn0, self.bn1 = bn0, bn1
-        self.tc = _lib.ENGINE == "tc" and rec.k <= 128 and c <= 8 and rec.kh * rec.kw <= 16
+        self.tc = _lib.ENGINE == "tc" and rec.k <= 128
         if not self.tc and (rec.k > 32 or rec.filters > 1024):
             raise AssertionError("planner chose the fused byte conv for an ineligible shape")
         self.w8 = _dev.widen_i8(self.w, rec.filters, rec.k) if self.tc else None
@@ -147,7 +147,9 @@ class _ByteConvFused(_Stage):
     def alloc(self, cap):
         super().alloc(cap)
         h, w, c = self.in_shape
-        self.codes = _dev.empty((cap * h * w,), np.uint8) if self.tc else None
+        r = self.rec
+        n = int(_lib.raw("b2_tc_byte_conv_scratch_bytes")(cap, h, w, c, r.kh, r.kw, r.stride, r.pad))
+        self.codes = _dev.empty((n,), np.uint8) if self.tc else None
 
     def launches(self):
         return 2 if self.tc else 1
@@ -528,8 +530,7 @@ class Network:
                 h, w, c = op["dims"]
                 conv = nxt if nxt is not None and nxt["kind"] == "conv" else None
                 crec = conv["rec"] if conv is not None else None
-                tc_ok = (_lib.ENGINE == "tc" and crec is not None and crec.k <= 128 and c <= 8
-                         and crec.kh * crec.kw <= 16)
+                tc_ok = _lib.ENGINE == "tc" and crec is not None and crec.k <= 128
                 kmax, fmax = (128, 1 << 30) if tc_ok else (32, 1024)
                 if (conv is not None and not op["flat"] and conv["rec"].k <= kmax and 1 < conv["rec"].filters <= fmax
                         and nxt2 is not None and nxt2["kind"] == "bn"

@@ -139,7 +139,7 @@ def test_tc_input8_bn_pack_vs_oracle(oracle, batch, units, k):
 
 
 @pytest.mark.parametrize("h,w,c,f,kh,pad,stride,pool", [(32, 32, 3, 128, 3, 1, 1, False), (16, 12, 3, 64, 3, 1, 1, True),
-                                                        (9, 9, 4, 200, 3, 2, 2, False), (8, 8, 8, 32, 3, 1, 1, True),
+                                                        (9, 9, 4, 200, 5, 2, 2, False), (8, 8, 14, 32, 3, 1, 1, True),
                                                         (5, 7, 1, 10, 3, 0, 1, False)])
 def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, pool):
     rng = np.random.default_rng(h * w + c + f)
@@ -169,7 +169,7 @@ def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, poo
     w8 = _dev.widen_i8(_dev.upload(wt), f, k)
     sites = ho * wo // (4 if pool else 1)
     out = _dev.empty((batch, sites, -(-f // 64)), np.uint64)
-    codes = _dev.empty((batch * h * w,), np.uint8)
+    codes = _dev.empty((_lib.raw("b2_tc_byte_conv_scratch_bytes")(batch, h, w, c, kh, kh, stride, pad),), np.uint8)
     _lib.call("b2_tc_byte_conv_bn_pack", _dev.P(_dev.upload(imgs)), batch, h, w, c, th(cal0), _dev.P(w8), f, kh, kh,
               stride, pad, int(pool), th(cal1), _dev.P(codes), _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))

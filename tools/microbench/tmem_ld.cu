@@ -1,0 +1,82 @@
+// TMEM -> register bandwidth of tcgen05.ld on B200: W warps per CTA (one
+// CTA per SM), each repeatedly loading 32 lanes x C columns of 32 bits.
+// Prints bytes/clk/SM for several warp counts and load widths.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdint.h>
+
+template <int X>
+__device__ __forceinline__ void ld(uint32_t taddr, uint32_t* v);
+template <>
+__device__ __forceinline__ void ld<16>(uint32_t a, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void ld<32>(uint32_t a, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,"
+      "%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(a));
+}
+
+template <int X>
+__global__ void k(int iters, uint32_t* sink, long long* clk) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t base = slot + ((uint32_t)((warp & 3) * 32) << 16);
+  uint32_t acc = 0, v[32];
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    const uint32_t col = ((i * X) + (warp >> 2) * 128) & 511;
+    ld<X>(base + col, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+    for (int j = 0; j < X; ++j) acc ^= v[j];
+  }
+  long long t1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  if (acc == 0x12345678) sink[0] = acc;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+}
+
+int main() {
+  uint32_t* sink;
+  long long* clk;
+  cudaMalloc(&sink, 4);
+  cudaMalloc(&clk, 148 * 8);
+  const int iters = 4096;
+  for (int warps : {4, 8, 16}) {
+    for (int x : {16, 32}) {
+      auto kern = x == 16 ? k<16> : k<32>;
+      kern<<<148, warps * 32>>>(iters, sink, clk);
+      cudaDeviceSynchronize();
+      long long c[148];
+      cudaMemcpy(c, clk, sizeof(c), cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (int i = 0; i < 148; ++i) avg += c[i];
+      avg /= 148;
+      double bytes = (double)iters * warps * 32 * x * 4;
+      printf("{\"test\": \"tcgen05.ld 32x32b.x%d\", \"warps\": %d, \"bytes_per_clk_per_sm\": %.1f, \"err\": \"%s\"}\n", x,
+             warps, bytes / avg, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}

@@ -23,7 +23,7 @@ from paper_1705_07175_b200.network import Network  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="bcnn", choices=["bcnn", "bmlp"])
-    ap.add_argument("--stage", type=int, default=0)
+    ap.add_argument("--stage", type=int, default=0, help="stage index, -1 = all")
     ap.add_argument("--batch", type=int, default=8192)
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
@@ -34,11 +34,17 @@ def main():
     net.input_device.copy_(torch.from_numpy(rng.integers(0, 256, (a.batch, n), dtype=np.uint8)).cuda())
     net.run(a.batch)
     torch.cuda.synchronize()
-    st = net.stages[a.stage]
-    for _ in range(a.reps):
+    stages = range(len(net.stages)) if a.stage < 0 else [a.stage]
+    for i in stages:
+        st = net.stages[i]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st.launch(net, a.batch, _dev.stream())
-    torch.cuda.synchronize()
-    print("stage", a.stage, st.name, "launches/stage", st.launches())
+        e0.record()
+        for _ in range(a.reps):
+            st.launch(net, a.batch, _dev.stream())
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"stage {i} {st.name}: {e0.elapsed_time(e1) / a.reps:.4f} ms  launches/stage {st.launches()}")
 
 
 if __name__ == "__main__":
