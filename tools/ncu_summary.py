@@ -2,6 +2,13 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv > profiles/xxx_launches.md
     python tools/ncu_summary.py full gpurun_out/prof.ncu-rep > profiles/xxx_full.md
+    python tools/ncu_summary.py traffic gpurun_out/traffic.csv gpurun_out/stage_map.json > profiles/traffic_bcnn.json
+
+`traffic` joins an ncu metrics list (dram__bytes_read/write.sum,
+gpu__time_duration.sum over `tools/profile_stage.py --map`) with the stage
+map that script wrote: our kernels are counted in launch order (namespace
+b2::, every launch of the library increments b2_launch_count), so the
+library launch index of each ncu row is its position among b2:: kernels.
 """
 import csv
 import io
@@ -60,5 +67,42 @@ def full(path):
         print()
 
 
+def traffic(csv_path, map_path):
+    import json
+    lines = open(csv_path).read().splitlines()
+    start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    per = defaultdict(dict)  # ncu launch ID -> metrics
+    names = {}
+    for r in rows:
+        lid = int(r["ID"])
+        names[lid] = r.get("Kernel Name", "")
+        try:
+            v = float(r["Metric Value"].replace(",", ""))
+        except (KeyError, ValueError):
+            continue
+        unit = r.get("Metric Unit", "")
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "usecond": 1e3,
+                "ms": 1e6, "msecond": 1e6, "nsecond": 1}.get(unit, 1)
+        per[lid][r["Metric Name"]] = v * mult
+    # ncu drops the outer b2:: namespace; everything that is not a torch /
+    # library kernel is ours
+    foreign = ("at::", "cutlass", "nccl", "cublas", "void at::")
+    ours = [lid for lid in sorted(per) if not any(f in names[lid] for f in foreign)]
+    smap = json.load(open(map_path))
+    base = smap["spans"]["0"]["first"]
+    # the map's launches are the LAST len(map) b2:: launches of the capture
+    total = max(sp["last"] for sp in smap["spans"].values()) - base
+    ours = ours[-total:]
+    out = {}
+    for k, sp in smap["spans"].items():
+        ids = ours[sp["first"] - base:sp["last"] - base]
+        out[k] = {"stage": sp["stage"], "batch": smap["batch"], "kernels": [names[i][:80] for i in ids],
+                  "dram_bytes": int(sum(per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0)
+                                        for i in ids)),
+                  "ncu_ns": int(sum(per[i].get("gpu__time_duration.sum", 0) for i in ids))}
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--stage", type=int, default=0, help="stage index, -1 = all")
     ap.add_argument("--batch", type=int, default=8192)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--map", default=None, help="write {stage: [first, last) library launch index} JSON here "
+                                                 "(one untimed launch per stage, for tools/ncu_summary.py traffic)")
     a = ap.parse_args()
     spec = zoo.bcnn_spec() if a.workload == "bcnn" else zoo.bmlp_spec()
     net = Network(spec, max_batch=a.batch, use_graphs=False)
@@ -34,6 +36,17 @@ def main():
     net.input_device.copy_(torch.from_numpy(rng.integers(0, 256, (a.batch, n), dtype=np.uint8)).cuda())
     net.run(a.batch)
     torch.cuda.synchronize()
+    if a.map:
+        import json
+        from paper_1705_07175_b200 import _lib
+        spans = {}
+        for i, st in enumerate(net.stages):
+            c0 = _lib.launch_count()
+            st.launch(net, a.batch, _dev.stream())
+            spans[str(i)] = {"stage": st.name, "first": c0, "last": _lib.launch_count()}
+        torch.cuda.synchronize()
+        json.dump({"workload": a.workload, "batch": a.batch, "spans": spans}, open(a.map, "w"), indent=1)
+        return
     stages = range(len(net.stages)) if a.stage < 0 else [a.stage]
     for i in stages:
         st = net.stages[i]
