@@ -121,34 +121,46 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int AM, int EM>
-int launch_bn(const Args& g, const int8_t* b_i8, int64_t kpad, cudaStream_t st) {
+template <int BN, int AM, int EM, int NPW, int BKS>
+int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st) {
+  g.nkb = (int)((k + BKS - 1) / BKS);
+  g.klast = (int)(((k - 1) % BKS) / 32 + 1);
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, kpad, BN)) return rc;
-  auto kern = k_tc_gemm<BN, AM, EM>;
+  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS>;
+  constexpr int smem = smem_bytes<BN, AM, BKS>();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<BN, AM>());
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, NUM_THREADS, smem_bytes<BN, AM>(), st>>>(map, g);
+  kern<<<grid, num_threads<NPW>(), smem, st>>>(map, g);
   return launched();
 }
 
-// N <= 128: 128-column tiles with a double-buffered accumulator; otherwise
-// 256-column tiles (one M=128 x N=256 MMA per 32 K: half the A widening and
-// MMA issue per MAC, measured 1.7x faster on 16384^3).
+// N <= 128: 128-column tiles, double-buffered accumulator, 256-element K
+// stages (128-element when a producer's 4 words would straddle two conv
+// sites, for u8 rows, and for the one-block first conv); otherwise 256-column
+// tiles (one M=128 x N=256 MMA per 32 K: half the A widening per MAC) with
+// 128-element stages.  Two producer warps per TMEM lane quarter, one for the
+// first conv.
 template <int AM, int EM>
 int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k) {
   if (g.M == 0 || g.N == 0) return 0;
-  g.klast = (int)(((k - 1) % BK) / 32 + 1);
-  if (g.N <= 128) return launch_bn<128, AM, EM>(g, b_i8, kpad, st);
-  return launch_bn<256, AM, EM>(g, b_i8, kpad, st);
+  if (g.N > 128) return launch_bn<256, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
+  if constexpr (AM == A_BYTECONV) {
+    return launch_bn<128, AM, EM, 4, 128>(g, b_i8, kpad, k, st);
+  } else if constexpr (AM == A_BYTES) {
+    return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
+  } else {
+    if (AM == A_CONV && g.spw % 4 != 0) return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
+    return launch_bn<128, AM, EM, 8, 256>(g, b_i8, kpad, k, st);
+  }
 }
 
-inline int64_t kpad_of(int64_t k) { return (k + BK - 1) / BK * BK; }
+inline int64_t kpad_of(int64_t k) { return (k + KPAD - 1) / KPAD * KPAD; }
 
 inline bool conv_ok(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad) {
   return batch >= 0 && h >= 1 && w >= 1 && c >= 1 && filters >= 1 && filters <= INT32_MAX && kh >= 1 && kw >= 1 &&
@@ -206,7 +218,6 @@ int b2_tc_bgemm(const uint64_t* a, int64_t m, const int8_t* b_i8, int64_t n, int
   g.awords = (k + 31) / 32;
   g.M = m;
   g.N = (int)n;
-  g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   g.out_i32 = out;
   g.ldo = n;
   return tc::launch<tc::A_ROWS, tc::E_I32>(g, b_i8, tc::kpad_of(k), S(stream), k);
@@ -222,7 +233,6 @@ int b2_tc_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, in
   g.awords = (k + 31) / 32;
   g.M = batch;
   g.N = (int)units;
-  g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   tc::pack_args(g, th, out, units);
   return tc::launch<tc::A_ROWS, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
@@ -234,7 +244,6 @@ int b2_tc_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c
   tc::conv_args(g, lines, batch, h, w, c, kh, kw, stride, pad);
   const int64_t k = (int64_t)kh * kw * c;
   g.N = (int)filters;
-  g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   g.out_i32 = out;
   g.ldo = filters;
   return tc::launch<tc::A_CONV, tc::E_I32>(g, w_i8, tc::kpad_of(k), S(stream), k);
@@ -250,7 +259,6 @@ int b2_tc_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c
   if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
   const int64_t k = (int64_t)kh * kw * c;
   g.N = (int)filters;
-  g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   tc::pack_args(g, th, out, filters);
   if (pool) return tc::launch<tc::A_CONV, tc::E_POOLPACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
   return tc::launch<tc::A_CONV, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
@@ -265,7 +273,6 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
   g.awords = (int)(k / 4);
   g.M = batch;
   g.N = (int)units;
-  g.nkb = (int)(tc::kpad_of(k) / tc::BK);
   tc::pack_args(g, th, out, units);
   return tc::launch<tc::A_BYTES, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
@@ -300,8 +307,8 @@ int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c
   g.N = (int)filters;
   g.nkb = 1;
   tc::pack_args(g, th_out, out, filters);
-  if (pool) return tc::launch<tc::A_BYTECONV, tc::E_POOLPACK>(g, w_i8, tc::BK, S(stream), k);
-  return tc::launch<tc::A_BYTECONV, tc::E_PACK>(g, w_i8, tc::BK, S(stream), k);
+  if (pool) return tc::launch<tc::A_BYTECONV, tc::E_POOLPACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
+  return tc::launch<tc::A_BYTECONV, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 
 }  // extern "C"

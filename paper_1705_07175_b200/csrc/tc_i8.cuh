@@ -43,9 +43,8 @@ namespace b2 {
 namespace tc {
 
 constexpr int BM = 128;                 // tile rows = TMEM lanes
-constexpr int BK = 128;                 // int8 K per stage = one 128-byte swizzle atom
-constexpr int A_STAGE_COLS = BK / 4;    // 32 TMEM columns per A stage
-constexpr int NUM_THREADS = 512;
+constexpr int BK = 128;                 // int8 K of one 128-byte swizzle atom (a TMA box row)
+constexpr int KPAD = 256;               // weight rows are padded to a multiple of this
 constexpr int PF = 4;                   // A-producer prefetch depth (K blocks)
 
 // A operand sources: packed rows; implicit bit-im2col of NHWC-bits
@@ -63,8 +62,8 @@ struct Args {
   // ---- problem
   int64_t M;
   int N;
-  int nkb;    // K blocks of 128
-  int klast;  // K=32 MMAs carrying data in the last block (1..4)
+  int nkb;    // K stages (BKS elements each)
+  int klast;  // K=32 MMAs carrying data in the last stage (1..BKS/32)
   // ---- epilogue
   int32_t* out_i32;
   int64_t ldo;
@@ -122,6 +121,11 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
           smem_u32(smem_dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// Pull [p, p + bytes) into L2 ahead of the producers' gathers (bytes % 16 == 0).
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -238,7 +242,7 @@ __device__ __forceinline__ void widen32m(uint32_t x, uint32_t valid, uint32_t* o
 // 128-element K block): walks this CTA's (tile, K block) sequence.
 //   A_ROWS / A_CONV / A_BYTECONV: 64 packed bits (uint2) + validity
 //   A_BYTES:                      64 raw bytes (4 x uint4)
-template <int AM, bool POOLED>
+template <int AM, bool POOLED, int WS>  // WS = K words (32 elements) per stage
 struct ACursor {
   int64_t t;       // tile of the next fetch
   int kb;          // K block of the next fetch
@@ -260,7 +264,7 @@ struct ACursor {
       ix0 = ox * g.stride - g.pad;
       base = g.a + img * (int64_t)g.H * g.W * g.sstride;
       cell = dy = dx = 0;
-      within = 2 * half;
+      within = (WS / 2) * half;  // two producer warps per lane quarter
       while (within >= g.spw) within -= g.spw, step_cell(g);
     } else {
       base = g.a + (mok ? m : 0) * g.lda;
@@ -280,47 +284,62 @@ struct ACursor {
       t += step;
       tile_setup(g, mtiles, tiles, r, half);
     } else if constexpr (AM == A_CONV) {
-      within += 4;
+      within += WS;
       while (within >= g.spw) within -= g.spw, step_cell(g);
     }
   }
 
-  // packed-bit modes: x = 64 bits of K, vm = validity (all ones / zero, or
-  // per bit for A_BYTECONV)
-  __device__ __forceinline__ void fetch_bits(const Args& g, int half, uint2& x, uint2& vm) {
-    x = make_uint2(0, 0);
-    vm = make_uint2(0, 0);
+  // packed-bit modes: x = WPH words (32 bits each) of K starting at word
+  // 4 kb + WPH half, vm = validity (all ones / zero, or per bit for
+  // A_BYTECONV).  WPH = 2 (two producer warps per lane quarter) or 4 (one).
+  template <int WPH>
+  __device__ __forceinline__ void fetch_bits(const Args& g, int half, uint4& x, uint4& vm) {
+    x = make_uint4(0, 0, 0, 0);
+    vm = make_uint4(0, 0, 0, 0);
     if constexpr (AM == A_ROWS) {
-      const int w0 = kb * 4 + 2 * half;
+      const int w0 = kb * WS + WPH * half;
       if (mok) {
-        vm = make_uint2(~0u, ~0u);
+        vm = make_uint4(~0u, ~0u, ~0u, ~0u);
         const uint32_t* p = base + w0;
-        if (w0 + 2 <= g.awords && (g.lda & 1) == 0) {
-          x = __ldg(reinterpret_cast<const uint2*>(p));
+        if (WPH == 4 && w0 + 4 <= g.awords && (g.lda & 3) == 0) {
+          x = __ldg(reinterpret_cast<const uint4*>(p));
+        } else if (WPH == 2 && w0 + 2 <= g.awords && (g.lda & 1) == 0) {
+          const uint2 y = __ldg(reinterpret_cast<const uint2*>(p));
+          x.x = y.x, x.y = y.y;
         } else {
           if (w0 + 0 < g.awords) x.x = __ldg(p + 0);
           if (w0 + 1 < g.awords) x.y = __ldg(p + 1);
+          if (WPH == 4 && w0 + 2 < g.awords) x.z = __ldg(p + 2);
+          if (WPH == 4 && w0 + 3 < g.awords) x.w = __ldg(p + 3);
         }
       }
     } else if constexpr (AM == A_CONV) {
-      // two consecutive K words of one site (spw even)
+      // WPH consecutive K words of one site (spw % WPH == 0)
       const int iy = iy0 + dy, ix = ix0 + dx;
       if (mok && dy < g.kh && iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) {
-        vm = make_uint2(~0u, ~0u);
-        x = __ldg(reinterpret_cast<const uint2*>(base + ((int64_t)iy * g.W + ix) * g.sstride + within));
+        vm = make_uint4(~0u, ~0u, ~0u, ~0u);
+        const uint32_t* p = base + ((int64_t)iy * g.W + ix) * g.sstride + within;
+        if constexpr (WPH == 4) {
+          x = __ldg(reinterpret_cast<const uint4*>(p));
+        } else {
+          const uint2 y = __ldg(reinterpret_cast<const uint2*>(p));
+          x.x = y.x, x.y = y.y;
+        }
       }
     } else if constexpr (AM == A_BYTECONV) {
       // masked rows written by k_byte_unroll: awords bit words then awords
       // validity words per row (padding cells of the window -> byte 0)
-      const int w0 = kb * 4 + 2 * half;
+      const int w0 = kb * WS + WPH * half;
       if (mok) {
         const uint32_t* p = base + w0;
         if (w0 + 0 < g.awords) x.x = __ldg(p + 0), vm.x = __ldg(p + g.awords + 0);
         if (w0 + 1 < g.awords) x.y = __ldg(p + 1), vm.y = __ldg(p + g.awords + 1);
+        if (WPH == 4 && w0 + 2 < g.awords) x.z = __ldg(p + 2), vm.z = __ldg(p + g.awords + 2);
+        if (WPH == 4 && w0 + 3 < g.awords) x.w = __ldg(p + 3), vm.w = __ldg(p + g.awords + 3);
       }
     }
   }
-  // A_BYTES: bytes [128 kb + 64 half, +64) of the row (awords = valid words)
+  // A_BYTES: bytes [128 kb + 64 half, +64) of the row (awords = valid words; WS == 4)
   __device__ __forceinline__ void fetch_bytes(const Args& g, int half, uint4 (&x)[4]) {
     const int w0 = kb * 32 + 16 * half;
     const bool vec = (g.lda & 3) == 0;
@@ -348,17 +367,56 @@ struct ACursor {
 // allows (192 KB) so TMA runs >= 3 us ahead of the tensor cores.  The
 // first conv has one K block per tile, so its accumulator ring is deeper
 // (3 x 128) to hide the MMA -> epilogue hand-off, with a 4-stage A ring.
-template <int BN, int AM = A_ROWS>
-constexpr int a_stages() {
-  return AM == A_BYTECONV ? 4 : 8;
+// L2 prefetch of the input rows tile `t` will gather (implicit im2col:
+// the NHWC-bits rows oy0*stride-pad .. oy1*stride-pad+kh-1 of the tile's
+// images are one contiguous range; packed rows: the tile's A rows).
+template <int AM>
+__device__ __forceinline__ void prefetch_tile_inputs(const Args& g, int64_t t, int64_t mtiles, int64_t tiles) {
+  if (t >= tiles) return;
+  const int64_t m0 = (t % mtiles) * BM;
+  const int64_t m1 = (m0 + BM < g.M ? m0 + BM : g.M) - 1;
+  int64_t lo, hi;  // uint32 word range
+  if constexpr (AM == A_CONV) {
+    // pool-ordered rows stay within the same output-row band as natural ones
+    const int64_t hw = (int64_t)g.Ho * g.Wo;
+    const int64_t i0 = m0 / hw, i1 = m1 / hw;
+    const int oy0 = (int)((m0 - i0 * hw) / g.Wo), oy1 = (int)((m1 - i1 * hw) / g.Wo);
+    int y0 = oy0 * g.stride - g.pad, y1 = oy1 * g.stride - g.pad + g.kh;
+    y0 = y0 < 0 ? 0 : y0;
+    y1 = y1 > g.H ? g.H : y1;
+    lo = (i0 * g.H + y0) * (int64_t)g.W * g.sstride;
+    hi = (i1 * g.H + y1) * (int64_t)g.W * g.sstride;
+  } else {
+    lo = m0 * g.lda;
+    hi = (m1 + 1) * g.lda;
+  }
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(g.a + lo);
+  int64_t bytes = (hi - lo) * 4;
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(p) & 15;
+  p -= mis;
+  bytes = (bytes + mis + 15) & ~int64_t(15);
+  while (bytes > 0) {
+    const uint32_t n = bytes > (1 << 20) ? (1u << 20) : (uint32_t)bytes;
+    l2_prefetch(p, n);
+    p += n;
+    bytes -= n;
+  }
 }
-template <int BN, int AM = A_ROWS>
-constexpr int b_stages() {
-  return (192 * 1024) / (BN * BK);  // 12 x 16 KB at BN = 128, 6 x 32 KB at BN = 256
-}
-template <int BN, int AM = A_ROWS>
+
+// K elements per pipeline stage (BKS): 256 for 128-column tiles (8 MMAs of
+// 64 cycles between the two ring commits — at 4 per stage the commits and
+// the issuing thread's waits cost ~40 % of the tensor pipe), else 128.
+template <int BN, int AM>
 constexpr int acc_bufs() {
   return BN > 128 ? 1 : (AM == A_BYTECONV ? 3 : 2);
+}
+template <int BN, int AM, int BKS>
+constexpr int a_stages() {  // TMEM: accumulators + A ring fill the 512 columns
+  return (512 - acc_bufs<BN, AM>() * BN) / (BKS / 4);
+}
+template <int BN, int BKS>
+constexpr int b_stages() {  // 192 KB of shared memory for the B ring
+  return (192 * 1024) / (BN * BKS);
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -389,12 +447,27 @@ __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncol
 }
 
 // ------------------------------------------------------------------ kernel
-template <int BN, int AM, int EM>
-__global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap, const Args g) {
+template <int NPW>
+constexpr int num_threads() {
+  return 32 * (4 + NPW + 4);
+}
+
+// NPW A-producer warps: 8 (two per TMEM lane quarter, 64 K elements each)
+// or 4 (one per quarter, the whole 128-element block: per-stage overheads
+// amortised over twice the widening, for 128-column tiles).
+template <int BN, int AM, int EM, int NPW, int BKS>
+__global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
+                                                                  const Args g) {
+  constexpr int WS = BKS / 32;        // K words per stage
+  constexpr int HALVES = NPW / 4;     // producer warps per lane quarter
+  constexpr int WPH = WS / HALVES;    // K words per producer thread per stage
+  constexpr int A_STAGE_COLS = BKS / 4;
+  constexpr int EPI0 = 4 + NPW;       // first epilogue warp
+  static_assert(WPH == 2 || WPH == 4, "producer word split");
   constexpr bool POOLED = (EM == E_POOLPACK);
-  constexpr int B_STAGE_BYTES = BN * BK;
-  constexpr int SA = a_stages<BN, AM>();
-  constexpr int SB = b_stages<BN, AM>();
+  constexpr int B_STAGE_BYTES = BN * BKS;
+  constexpr int SA = a_stages<BN, AM, BKS>();
+  constexpr int SB = b_stages<BN, BKS>();
   constexpr int ACC_COLS = BN;
   constexpr int ACC_BUFS = acc_bufs<BN, AM>();
   constexpr int A_COL0 = ACC_BUFS * ACC_COLS;
@@ -427,7 +500,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       mbar_init(&bempty[s], 1);
     }
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&full[s], 8);  // 8 A-producer warps
+      mbar_init(&full[s], NPW);  // every A-producer warp arrives
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < ACC_BUFS; ++a) {
@@ -451,12 +524,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      if constexpr (AM == A_CONV || AM == A_ROWS) {
+        prefetch_tile_inputs<AM>(g, blockIdx.x, mtiles, tiles);
+        prefetch_tile_inputs<AM>(g, blockIdx.x + gridDim.x, mtiles, tiles);
+      }
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int n0 = (int)(t / mtiles) * BN;
+        if constexpr (AM == A_CONV || AM == A_ROWS) prefetch_tile_inputs<AM>(g, t + 2 * (int64_t)gridDim.x, mtiles, tiles);
         for (int kb = 0; kb < g.nkb; ++kb) {
           mbar_wait(&bempty[s], ph ^ 1);
           mbar_expect_tx(&bfull[s], B_STAGE_BYTES);
-          tma_load_2d(sb + s * B_STAGE_BYTES, &bmap, &bfull[s], kb * BK, n0);
+#pragma unroll
+          for (int at = 0; at < BKS / BK; ++at)  // one 128-byte-wide box per swizzle atom
+            tma_load_2d(sb + s * B_STAGE_BYTES + at * BN * BK, &bmap, &bfull[s], kb * BKS + at * BK, n0);
           if (++s == SB) s = 0, ph ^= 1;
         }
       }
@@ -478,10 +558,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           tc_fence_after();
           const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
           const uint32_t bs = smem_u32(sb + sb_ * B_STAGE_BYTES);
-          const int kmma = kb + 1 == g.nkb ? g.klast : BK / 32;
+          const int kmma = kb + 1 == g.nkb ? g.klast : BKS / 32;
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k)
-            if (k < kmma) tc_mma_i8(d, a + k * 8, sw128_desc(bs + k * 32), IDESC, (kb | k) ? 1u : 0u);
+          for (int k = 0; k < BKS / 32; ++k)
+            if (k < kmma)
+              tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, (kb | k) ? 1u : 0u);
           tc_commit(&bempty[sb_]);
           tc_commit(&empty[s]);
           if (++s == SA) s = 0, ph ^= 1;
@@ -491,7 +572,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
         if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
       }
     }
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp >= 4 && warp < EPI0) {
     // ------------------------------------------------ A producers
     // Two warps per TMEM lane quarter, each producing half (64 elements) of
     // the row's 128-element K block.  The cursor runs PF K blocks ahead of
@@ -499,16 +580,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     // gathers overlap the widening and the TMEM stores; each stage is
     // published one iteration later, after its tcgen05.st has drained.
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
+    const int half = HALVES == 1 ? 0 : (warp - 4) >> 2;
     const int r = q * 32 + lane;  // tile row = TMEM lane
-    const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / 2);
-    ACursor<AM, POOLED> cur;
+    const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / HALVES);
+    ACursor<AM, POOLED, WS> cur;
     cur.start(g, blockIdx.x, mtiles, tiles, r, half);
     const int64_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int64_t jobs = my_tiles * g.nkb;
     int s = 0, pending = -1;
     uint32_t ph = 0;
-    auto publish = [&](int stage, uint32_t (&v)[16]) {
+    auto publish = [&](int stage, uint32_t (&v)[8 * WPH]) {
       if (pending >= 0) {
         tmem_wait_st();
         tc_fence_before();
@@ -518,11 +599,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       mbar_wait(&empty[stage], ph ^ 1);
       tc_fence_after();
 #ifndef B2_PROBE_SKIP_A
-      tmem_st16(st_addr + stage * A_STAGE_COLS, v);
+      if constexpr (WPH == 4)
+        tmem_st32(st_addr + stage * A_STAGE_COLS, v);
+      else
+        tmem_st16(st_addr + stage * A_STAGE_COLS, v);
 #endif
       pending = stage;
     };
     if constexpr (AM == A_BYTES) {
+      static_assert(NPW == 8 && WS == 4, "u8 rows: two producer warps per quarter, 128-element stages");
       uint4 qx[2][4];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -552,14 +637,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       // BYTECONV keeps a per-bit validity word per slot; the row and conv
       // modes only a flag (valid rows widen to +/-1, invalid ones to 0)
       constexpr bool MASKED = AM == A_BYTECONV;
-      uint2 qx[PF], qv[MASKED ? PF : 1];
+      uint4 qx[PF], qv[MASKED ? PF : 1];
       bool qok[PF];
 #pragma unroll
       for (int u = 0; u < PF; ++u) {
-        uint2 vm;
-        cur.fetch_bits(g, half, qx[u], vm);
+        uint4 vm;
+        cur.template fetch_bits<WPH>(g, half, qx[u], vm);
         if constexpr (MASKED) qv[u] = vm;
-        qok[u] = vm.x != 0 || vm.y != 0;
+        qok[u] = vm.x != 0 || vm.y != 0 || vm.z != 0 || vm.w != 0;
         cur.advance(g, gridDim.x, mtiles, tiles, r, half);
       }
       const int ijobs = (int)jobs;
@@ -567,22 +652,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
 #pragma unroll
         for (int u = 0; u < PF; ++u) {
           if (j0 + u < ijobs) {
-            uint32_t v[16];
+            uint32_t v[8 * WPH];
 #ifndef B2_PROBE_SKIP_A
             if constexpr (MASKED) {
               widen32m(qx[u].x, qv[u].x, v + 0);
               widen32m(qx[u].y, qv[u].y, v + 8);
+              if constexpr (WPH == 4) {
+                widen32m(qx[u].z, qv[u].z, v + 16);
+                widen32m(qx[u].w, qv[u].w, v + 24);
+              }
             } else {
               widen32(qx[u].x, qok[u], v + 0);
               widen32(qx[u].y, qok[u], v + 8);
+              if constexpr (WPH == 4) {
+                widen32(qx[u].z, qok[u], v + 16);
+                widen32(qx[u].w, qok[u], v + 24);
+              }
             }
 #endif
             // refill the slot only after it was consumed: the load lands in
             // the same registers and nothing waits on it until PF stages later
-            uint2 vm;
-            cur.fetch_bits(g, half, qx[u], vm);
+            uint4 vm;
+            cur.template fetch_bits<WPH>(g, half, qx[u], vm);
             if constexpr (MASKED) qv[u] = vm;
-            qok[u] = vm.x != 0 || vm.y != 0;
+            qok[u] = vm.x != 0 || vm.y != 0 || vm.z != 0 || vm.w != 0;
             cur.advance(g, gridDim.x, mtiles, tiles, r, half);
             publish(s, v);
             if (++s == SA) s = 0, ph ^= 1;
@@ -596,7 +689,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[pending]);
     }
-  } else if (warp >= 12) {
+  } else if (warp >= EPI0) {
     // ------------------------------------------------ epilogue
     const int q = warp & 3;
     const int r = q * 32 + lane;
@@ -714,10 +807,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   }
 }
 
-template <int BN, int AM>
+template <int BN, int AM, int BKS>
 constexpr int smem_bytes() {
-  return b_stages<BN, AM>() * BN * BK + THR_COLS * 8 + THR_COLS / 8 +
-         8 * (2 * b_stages<BN, AM>() + 2 * a_stages<BN, AM>() + 6) + 16 + 1024;
+  return b_stages<BN, BKS>() * BN * BKS + THR_COLS * 8 + THR_COLS / 8 +
+         8 * (2 * b_stages<BN, BKS>() + 2 * a_stages<BN, AM, BKS>() + 6) + 16 + 1024;
 }
 
 }  // namespace tc
