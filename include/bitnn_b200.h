@@ -222,7 +222,7 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
                          uint64_t* out, void* stream);
 
 /* _PackedByteBN -> _PackedConv [-> _Pool 2x2/2] -> _PackedBN, as
- * b2_byte_conv_bn_pack (kh*kw*c <= 128).  Two launches: the byte batchnorm
+ * b2_byte_conv_bn_pack (kh*kw*c <= 128, c <= 8).  Two launches: the byte batchnorm
  * + bit im2col (_kernels.py:170-199) of every output pixel into `scratch`
  * (b2_tc_byte_conv_scratch_bytes bytes: window bits plus a validity mask,
  * padding cells invalid), then the tensor-core GEMM with zero padding. */

@@ -36,49 +36,80 @@ __global__ void k_expand_i8(const uint64_t* __restrict__ w, int64_t rows, int64_
 }
 
 // network.py:128-138 _PackedByteBN on the raw image followed by the bit
-// im2col of _kernels.py:170-199 (unroll_packed), one thread per output
-// pixel: row = kw32 words of window bits (K order (dy, dx, c), c fastest)
-// then kw32 words of validity (0 for window cells in the padding ring, so
-// the tensor cores see zero padding and no correction map is needed).
-__global__ void k_byte_unroll(const uint8_t* __restrict__ x, int64_t rows, int h, int w, int c, int kh, int kw,
-                              int stride, int pad, int ho, int wo, int kw32, int pooled,
-                              const int32_t* __restrict__ t, const uint8_t* __restrict__ ge,
-                              uint32_t* __restrict__ out) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int64_t hw = (int64_t)ho * wo;
-  const int64_t img = r / hw;
-  const int pos = (int)(r - img * hw);
-  int oy, ox;
-  if (pooled) {  // pool-window-major rows, as tc::row_pos<true>
-    const int q = pos >> 2, cell = pos & 3, wp = wo >> 1;
-    oy = 2 * (q / wp) + (cell >> 1);
-    ox = 2 * (q % wp) + (cell & 1);
-  } else {
-    oy = pos / wo;
-    ox = pos - oy * wo;
-  }
+// im2col of _kernels.py:170-199 (unroll_packed): row = kw32 words of window
+// bits (K order (dy, dx, c), c fastest) then kw32 words of validity (0 for
+// window cells in the padding ring, so the tensor cores see zero padding
+// and no correction map is needed).  Rows are ordered like the conv output
+// (pool-window-major when `pooled`).
+//
+// One CTA per (image, band of BAND output rows): the byte batchnorm code of
+// every input site the band touches (c <= 8 bits) is computed once into
+// shared memory, then each thread assembles its pixels' windows from there.
+constexpr int BAND = 8;
+
+__device__ __forceinline__ int64_t unroll_row(int64_t img, int oy, int ox, int ho, int wo, int pooled) {
+  if (!pooled) return (img * ho + oy) * (int64_t)wo + ox;
+  const int wp = wo >> 1;
+  const int q = (oy >> 1) * wp + (ox >> 1);
+  return img * (int64_t)ho * wo + 4 * q + 2 * (oy & 1) + (ox & 1);
+}
+
+__global__ void __launch_bounds__(256) k_byte_unroll(const uint8_t* __restrict__ x, int h, int w, int c, int kh, int kw,
+                                                     int stride, int pad, int ho, int wo, int kw32, int pooled,
+                                                     const int32_t* __restrict__ t, const uint8_t* __restrict__ ge,
+                                                     uint32_t* __restrict__ out) {
+  extern __shared__ uint8_t codes[];  // [in_rows][w]
+  const int64_t img = blockIdx.y;
+  const int oy0 = blockIdx.x * BAND;
+  const int oy1 = min(oy0 + BAND, ho);
+  const int iy0 = oy0 * stride - pad;
+  const int in_rows = (oy1 - 1 - oy0) * stride + kh;
   const uint8_t* xi = x + img * (int64_t)h * w * c;
-  uint32_t bits[4] = {0, 0, 0, 0}, valid[4] = {0, 0, 0, 0};
-  int p = 0;
-  for (int dy = 0; dy < kh; ++dy) {
-    const int iy = oy * stride + dy - pad;
-    for (int dx = 0; dx < kw; ++dx) {
-      const int ix = ox * stride + dx - pad;
-      const bool ok = iy >= 0 && iy < h && ix >= 0 && ix < w;
+  int32_t tc[8];
+  bool gc[8];
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    tc[ch] = ch < c ? __ldg(t + ch) : 0;
+    gc[ch] = ch < c ? __ldg(ge + ch) != 0 : true;
+  }
+  for (int i = threadIdx.x; i < in_rows * w; i += blockDim.x) {
+    const int iy = iy0 + i / w, ix = i % w;
+    uint32_t code = 0;
+    if (iy >= 0 && iy < h) {
       const uint8_t* px = xi + ((int64_t)iy * w + ix) * c;
-      for (int ch = 0; ch < c; ++ch, ++p) {
-        if (!ok) continue;
-        const bool b = thr_bit((int32_t)__ldg(px + ch), __ldg(t + ch), __ldg(ge + ch) != 0);
-        bits[p >> 5] |= (uint32_t)b << (p & 31);
-        valid[p >> 5] |= 1u << (p & 31);
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        if (ch < c) code |= (uint32_t)thr_bit((int32_t)px[ch], tc[ch], gc[ch]) << ch;
+    }
+    codes[i] = (uint8_t)code;
+  }
+  __syncthreads();
+  const uint32_t cmask = (1u << c) - 1u;
+  for (int p = threadIdx.x; p < (oy1 - oy0) * wo; p += blockDim.x) {
+    const int oy = oy0 + p / wo, ox = p % wo;
+    uint32_t bits[4] = {0, 0, 0, 0}, valid[4] = {0, 0, 0, 0};
+    int pos = 0;
+    for (int dy = 0; dy < kh; ++dy) {
+      const int iy = oy * stride + dy - pad;
+      const int srow = (iy - iy0) * w;
+      for (int dx = 0; dx < kw; ++dx, pos += c) {
+        const int ix = ox * stride + dx - pad;
+        if (iy < 0 || iy >= h || ix < 0 || ix >= w) continue;
+        const uint32_t code = codes[srow + ix];
+        const int wd = pos >> 5, sh = pos & 31;
+        bits[wd] |= code << sh;
+        valid[wd] |= cmask << sh;
+        if (sh + c > 32) {  // a site straddling two words
+          bits[wd + 1] |= code >> (32 - sh);
+          valid[wd + 1] |= cmask >> (32 - sh);
+        }
       }
     }
-  }
-  uint32_t* o = out + r * 2 * kw32;
-  for (int i = 0; i < kw32; ++i) {
-    o[i] = bits[i];
-    o[kw32 + i] = valid[i];
+    uint32_t* o = out + unroll_row(img, oy, ox, ho, wo, pooled) * 2 * kw32;
+    for (int i = 0; i < kw32; ++i) {
+      o[i] = bits[i];
+      o[kw32 + i] = valid[i];
+    }
   }
 }
 
@@ -121,13 +152,13 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int AM, int EM, int NPW, int BKS>
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4)>
 int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st) {
   g.nkb = (int)((k + BKS - 1) / BKS);
   g.klast = (int)(((k - 1) % BKS) / 32 + 1);
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, kpad, BN)) return rc;
-  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS>;
+  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI>;
   constexpr int smem = smem_bytes<BN, AM, BKS>();
   static bool attr = false;
   if (!attr) {
@@ -136,7 +167,7 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   }
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, num_threads<NPW>(), smem, st>>>(map, g);
+  kern<<<grid, num_threads<NPW, NEPI>(), smem, st>>>(map, g);
   return launched();
 }
 
@@ -151,7 +182,7 @@ int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k)
   if (g.M == 0 || g.N == 0) return 0;
   if (g.N > 128) return launch_bn<256, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
   if constexpr (AM == A_BYTECONV) {
-    return launch_bn<128, AM, EM, 4, 128>(g, b_i8, kpad, k, st);
+    return launch_bn<128, AM, EM, 4, 128, 8>(g, b_i8, kpad, k, st);
   } else if constexpr (AM == A_BYTES) {
     return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
   } else {
@@ -287,7 +318,7 @@ int64_t b2_tc_byte_conv_scratch_bytes(int64_t batch, int h, int w, int c, int kh
 int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
                             const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
                             b2_thresh th_out, void* scratch, uint64_t* out, void* stream) {
-  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > tc::BK || !scratch ||
+  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > tc::BK || c > 8 || !scratch ||
       !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir)
     return B2_EINVAL;
   tc::Args g{};
@@ -296,9 +327,15 @@ int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c
   if (!batch) return 0;
   const int64_t k = (int64_t)kh * kw * c;
   const int kw32 = (int)((k + 31) / 32);
-  tc::k_byte_unroll<<<(unsigned)cdiv(g.M, 256), 256, 0, S(stream)>>>(x, g.M, h, w, c, kh, kw, stride, pad, g.Ho,
-                                                                     g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
-                                                                     reinterpret_cast<uint32_t*>(scratch));
+  {
+    const int bands = (g.Ho + tc::BAND - 1) / tc::BAND;
+    const int in_rows = (tc::BAND - 1) * stride + kh;
+    const size_t smem = (size_t)in_rows * w;
+    if (smem > 48 * 1024 || batch > 65535) return B2_EINVAL;
+    tc::k_byte_unroll<<<dim3((unsigned)bands, (unsigned)batch), 256, smem, S(stream)>>>(
+        x, h, w, c, kh, kw, stride, pad, g.Ho, g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
+        reinterpret_cast<uint32_t*>(scratch));
+  }
   if (int rc = launched()) return rc;
   // rows are ordered like the conv output (pool-window-major when pooled)
   g.a = reinterpret_cast<const uint32_t*>(scratch);

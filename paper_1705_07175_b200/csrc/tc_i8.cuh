@@ -419,17 +419,21 @@ constexpr int b_stages() {  // 192 KB of shared memory for the B ring
   return (192 * 1024) / (BN * BKS);
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+template <int NEPI>
+__device__ __forceinline__ void epi_bar() {  // named barrier of the epilogue warps
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
+}
 
 constexpr int THR_COLS = 2048;  // resident threshold table (columns)
 
-// Threshold table for columns [n0, n0 + ncols) (ncols % 128 == 0), built by
-// the 128 epilogue threads: ge -> (1, -t), le -> (-1, t), column beyond N ->
-// (0, -1) = bit 0; one ge-direction mask word per 32 columns (ballot).
-__device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncols, int r, int lane, int4* sthr,
-                                                 uint32_t* sgm) {
+// Threshold table for columns [n0, n0 + ncols) (ncols % nthr == 0), built
+// by the nthr epilogue threads (et = 0 .. nthr-1): ge -> (1, -t), le ->
+// (-1, t), column beyond N -> (0, -1) = bit 0; one ge-direction mask word
+// per 32 columns (ballot).
+__device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncols, int et, int nthr, int lane,
+                                                 int4* sthr, uint32_t* sgm) {
   int* st = reinterpret_cast<int*>(sthr);
-  for (int j = r; j < ncols; j += 128) {
+  for (int j = et; j < ncols; j += nthr) {
     const int n = n0 + j;
     int mul = 0, add = -1;
     bool ge = true;
@@ -447,16 +451,20 @@ __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncol
 }
 
 // ------------------------------------------------------------------ kernel
-template <int NPW>
+template <int NPW, int NEPI>
 constexpr int num_threads() {
-  return 32 * (4 + NPW + 4);
+  return 32 * (4 + NPW + NEPI);
 }
 
 // NPW A-producer warps: 8 (two per TMEM lane quarter, 64 K elements each)
 // or 4 (one per quarter, the whole 128-element block: per-stage overheads
 // amortised over twice the widening, for 128-column tiles).
-template <int BN, int AM, int EM, int NPW, int BKS>
-__global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
+// NEPI epilogue warps: 4 (one per lane quarter, all columns) or 8 (two per
+// quarter, half the columns each: TMEM reads are latency-bound per warp,
+// ~42 B/clk each, so a single-buffered 256-column accumulator drains twice
+// as fast).
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI>
+__global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
                                                                   const Args g) {
   constexpr int WS = BKS / 32;        // K words per stage
   constexpr int HALVES = NPW / 4;     // producer warps per lane quarter
@@ -505,7 +513,7 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
     }
     for (int a = 0; a < ACC_BUFS; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], NEPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
@@ -691,9 +699,13 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
     }
   } else if (warp >= EPI0) {
     // ------------------------------------------------ epilogue
-    const int q = warp & 3;
+    constexpr int ECOLS = BN / (NEPI / 4);  // columns per epilogue warp
+    constexpr int ECH = ECOLS / 32;         // 32-column chunks per epilogue warp
+    const int q = warp & 3;                 // EPI0 % 4 == 0: lane quarter
     const int r = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const int ec0 = ((warp - EPI0) >> 2) * ECOLS;  // first tile column of this warp
+    const int et = (warp - EPI0) * 32 + lane;
+    const uint32_t lane_addr = ((uint32_t)(q * 32) << 16) + ec0;
     int acc = 0;
     uint32_t aph = 0;
     // thresholds as bit = (acc * mul + add >= 0), resident for the launch
@@ -702,8 +714,8 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
     const bool static_thr = ncols <= THR_COLS;
     if constexpr (EM != E_I32) {
       if (static_thr) {
-        stage_thresholds(g, 0, ncols, r, lane, sthr, sgm);
-        epi_bar();
+        stage_thresholds(g, 0, ncols, et, 32 * NEPI, lane, sthr, sgm);
+        epi_bar<NEPI>();
       }
     }
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -713,9 +725,9 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
       const bool mok = m < g.M;
       if constexpr (EM != E_I32) {
         if (!static_thr) {  // N too wide for the resident table: this tile's columns only
-          epi_bar();
-          stage_thresholds(g, n0, BN, r, lane, sthr, sgm);
-          epi_bar();
+          epi_bar<NEPI>();
+          stage_thresholds(g, n0, BN, et, 32 * NEPI, lane, sthr, sgm);
+          epi_bar<NEPI>();
         }
       }
 #ifdef B2_EPI_SLEEP
@@ -724,19 +736,19 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
       mbar_wait(&tfull[acc], aph);
 #endif
       tc_fence_after();
-      uint32_t words[BN / 32];
-      const int4* trow = sthr + (tcol >> 1);  // (mul, add) pairs of this tile's columns
+      uint32_t words[ECH];
+      const int4* trow = sthr + ((tcol + ec0) >> 1);  // (mul, add) pairs of this warp's columns
       // TMEM -> registers, software-pipelined: chunk c + 1 is in flight while
       // chunk c is thresholded (tcgen05.wait::ld waits for all prior loads)
       uint32_t va[32], vb[32];
       tmem_ld32(tmem + lane_addr + acc * ACC_COLS, va);
       tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < ECH; ++c) {
         uint32_t(&v)[32] = (c & 1) ? vb : va;
         uint32_t(&vn)[32] = (c & 1) ? va : vb;
-        if (c + 1 < BN / 32) tmem_ld32(tmem + lane_addr + acc * ACC_COLS + (c + 1) * 32, vn);
-        const int nb = n0 + c * 32;
+        if (c + 1 < ECH) tmem_ld32(tmem + lane_addr + acc * ACC_COLS + (c + 1) * 32, vn);
+        const int nb = n0 + ec0 + c * 32;
         if constexpr (EM == E_I32) {
           if (mok && nb < g.N) {
             int32_t* o = g.out_i32 + m * g.ldo + nb;
@@ -765,7 +777,7 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
           if constexpr (EM == E_POOLPACK) {
             // max over the 2x2 window then threshold == OR (ge) / AND (le)
             // of the four thresholded rows (monotone threshold)
-            const uint32_t gm = sgm[(tcol >> 5) + c];
+            const uint32_t gm = sgm[((tcol + ec0) >> 5) + c];
             uint32_t o = w | __shfl_xor_sync(0xffffffffu, w, 1);
             o |= __shfl_xor_sync(0xffffffffu, o, 2);
             uint32_t a = w & __shfl_xor_sync(0xffffffffu, w, 1);
@@ -774,7 +786,7 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
           }
           words[c] = w;
         }
-        if (c + 1 < BN / 32) tmem_wait_ld();
+        if (c + 1 < ECH) tmem_wait_ld();
       }
       tc_fence_before();
       __syncwarp();
@@ -783,15 +795,16 @@ __global__ void __launch_bounds__(num_threads<NPW>(), 1) k_tc_gemm(const __grid_
         const int64_t site = POOLED ? (m >> 2) : m;
         const bool writer = mok && (!POOLED || (lane & 3) == 0);
         if (writer) {
-          uint32_t* o = g.out_bits + site * g.ldo32 + n0 / 32;
-          if (n0 / 32 + BN / 32 <= g.ldo32 && (g.ldo32 & 3) == 0) {
+          const int w0 = (n0 + ec0) / 32;
+          uint32_t* o = g.out_bits + site * g.ldo32 + w0;
+          if (w0 + ECH <= g.ldo32 && (g.ldo32 & 3) == 0) {
 #pragma unroll
-            for (int c = 0; c < BN / 32; c += 4)
+            for (int c = 0; c < ECH; c += 4)
               *reinterpret_cast<uint4*>(o + c) = make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c)
-              if (n0 / 32 + c < g.ldo32) o[c] = words[c];
+            for (int c = 0; c < ECH; ++c)
+              if (w0 + c < g.ldo32) o[c] = words[c];
           }
         }
       }

@@ -136,7 +136,7 @@ class _ByteConvFused(_Stage):
         self.w_out = (w + 2 * rec.pad - rec.kw) // rec.stride + 1
         self.w = _dev.upload(rec.words)
         self.bn0, self.bn1 = bn0, bn1
-        self.tc = _lib.ENGINE == "tc" and rec.k <= 128
+        self.tc = _lib.ENGINE == "tc" and rec.k <= 128 and c <= 8
         if not self.tc and (rec.k > 32 or rec.filters > 1024):
             raise AssertionError("planner chose the fused byte conv for an ineligible shape")
         self.w8 = _dev.widen_i8(self.w, rec.filters, rec.k) if self.tc else None
@@ -530,7 +530,7 @@ class Network:
                 h, w, c = op["dims"]
                 conv = nxt if nxt is not None and nxt["kind"] == "conv" else None
                 crec = conv["rec"] if conv is not None else None
-                tc_ok = _lib.ENGINE == "tc" and crec is not None and crec.k <= 128
+                tc_ok = _lib.ENGINE == "tc" and crec is not None and crec.k <= 128 and c <= 8
                 kmax, fmax = (128, 1 << 30) if tc_ok else (32, 1024)
                 if (conv is not None and not op["flat"] and conv["rec"].k <= kmax and 1 < conv["rec"].filters <= fmax
                         and nxt2 is not None and nxt2["kind"] == "bn"

@@ -139,7 +139,7 @@ def test_tc_input8_bn_pack_vs_oracle(oracle, batch, units, k):
 
 
 @pytest.mark.parametrize("h,w,c,f,kh,pad,stride,pool", [(32, 32, 3, 128, 3, 1, 1, False), (16, 12, 3, 64, 3, 1, 1, True),
-                                                        (9, 9, 4, 200, 5, 2, 2, False), (8, 8, 14, 32, 3, 1, 1, True),
+                                                        (9, 9, 4, 200, 5, 2, 2, False), (8, 8, 8, 32, 3, 1, 1, True), (10, 6, 5, 64, 5, 2, 1, True),
                                                         (5, 7, 1, 10, 3, 0, 1, False)])
 def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, pool):
     rng = np.random.default_rng(h * w + c + f)

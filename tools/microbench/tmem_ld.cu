@@ -26,6 +26,23 @@ __device__ __forceinline__ void ld<32>(uint32_t a, uint32_t* v) {
       : "r"(a));
 }
 
+template <>
+__device__ __forceinline__ void ld<64>(uint32_t a, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,"
+      "%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,"
+      "%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]),
+        "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]),
+        "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]),
+        "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]),
+        "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+      : "r"(a));
+}
+
 template <int X>
 __global__ void k(int iters, uint32_t* sink, long long* clk) {
   __shared__ uint32_t slot;
@@ -39,7 +56,7 @@ __global__ void k(int iters, uint32_t* sink, long long* clk) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t base = slot + ((uint32_t)((warp & 3) * 32) << 16);
-  uint32_t acc = 0, v[32];
+  uint32_t acc = 0, v[64];
   long long t0 = clock64();
   for (int i = 0; i < iters; ++i) {
     const uint32_t col = ((i * X) + (warp >> 2) * 128) & 511;
@@ -63,9 +80,9 @@ int main() {
   cudaMalloc(&sink, 4);
   cudaMalloc(&clk, 148 * 8);
   const int iters = 4096;
-  for (int warps : {4, 8, 16}) {
-    for (int x : {16, 32}) {
-      auto kern = x == 16 ? k<16> : k<32>;
+  for (int warps : {4, 8, 12, 16}) {
+    for (int x : {16, 32, 64}) {
+      auto kern = x == 16 ? k<16> : (x == 32 ? k<32> : k<64>);
       kern<<<148, warps * 32>>>(iters, sink, clk);
       cudaDeviceSynchronize();
       long long c[148];
