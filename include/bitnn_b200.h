@@ -184,7 +184,7 @@ int b2_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b
  * correction map (layers.py:224-252) implicit: conv results already equal
  * conv_forward's "bgemm + correction". */
 
-/* K rounded up to the 256-element granule of the tcgen05 int8 GEMM's weight rows. */
+/* K rounded up to the 512-element granule of the tcgen05 int8 GEMM weight rows. */
 int64_t b2_i8_kpad(int64_t k);
 
 /* Widen packed +/-1 lines to int8 for the tensor pipe (_kernels.py:57-64

@@ -171,8 +171,9 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   return launched();
 }
 
-// N <= 128: 128-column tiles, double-buffered accumulator, 256-element K
-// stages (128-element when a producer's 4 words would straddle two conv
+// N <= 128: 128-column tiles, double-buffered accumulator, 512-element K
+// stages (16 MMAs of 64 cycles per stage hide the issuing thread's per-stage
+// wait + commit, tools/microbench/mma_loop.cu) (128-element when a producer's 4 words would straddle two conv
 // sites, for u8 rows, and for the one-block first conv); otherwise 256-column
 // tiles (one M=128 x N=256 MMA per 32 K: half the A widening per MAC) with
 // 128-element stages.  Two producer warps per TMEM lane quarter, one for the
@@ -187,11 +188,12 @@ int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k)
     return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
   } else {
     if (AM == A_CONV && g.spw % 4 != 0) return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
-    return launch_bn<128, AM, EM, 8, 256>(g, b_i8, kpad, k, st);
+    return launch_bn<128, AM, EM, 8, 512>(g, b_i8, kpad, k, st);
   }
 }
 
 inline int64_t kpad_of(int64_t k) { return (k + KPAD - 1) / KPAD * KPAD; }
+static_assert(KPAD % 128 == 0, "weight rows pad to whole TMA boxes");
 
 inline bool conv_ok(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad) {
   return batch >= 0 && h >= 1 && w >= 1 && c >= 1 && filters >= 1 && filters <= INT32_MAX && kh >= 1 && kw >= 1 &&

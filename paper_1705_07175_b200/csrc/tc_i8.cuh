@@ -44,7 +44,7 @@ namespace tc {
 
 constexpr int BM = 128;                 // tile rows = TMEM lanes
 constexpr int BK = 128;                 // int8 K of one 128-byte swizzle atom (a TMA box row)
-constexpr int KPAD = 256;               // weight rows are padded to a multiple of this
+constexpr int KPAD = 512;               // weight rows are padded to a multiple of the widest stage
 constexpr int PF = 4;                   // A-producer prefetch depth (K blocks)
 
 // A operand sources: packed rows; implicit bit-im2col of NHWC-bits
@@ -163,6 +163,11 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
       B2_R32(v)
       : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
@@ -339,6 +344,48 @@ struct ACursor {
       }
     }
   }
+  // 8 words (two 4-word chunks) per producer thread: 512-element stages.
+  // ok[j] = chunk j lies inside the operand (conv: its site is in bounds).
+  __device__ __forceinline__ void fetch_bits8(const Args& g, int half, uint4 (&x)[2], bool (&ok)[2]) {
+    x[0] = x[1] = make_uint4(0, 0, 0, 0);
+    ok[0] = ok[1] = false;
+    if constexpr (AM == A_ROWS) {
+      const int w0 = kb * WS + 8 * half;
+      ok[0] = ok[1] = mok;
+      if (mok) {
+        const uint32_t* p = base + w0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int w = w0 + 4 * j;
+          if (w + 4 <= g.awords && (g.lda & 3) == 0) {
+            x[j] = __ldg(reinterpret_cast<const uint4*>(p + 4 * j));
+          } else {
+            if (w + 0 < g.awords) x[j].x = __ldg(p + 4 * j + 0);
+            if (w + 1 < g.awords) x[j].y = __ldg(p + 4 * j + 1);
+            if (w + 2 < g.awords) x[j].z = __ldg(p + 4 * j + 2);
+            if (w + 3 < g.awords) x[j].w = __ldg(p + 4 * j + 3);
+          }
+        }
+      }
+    } else if constexpr (AM == A_CONV) {
+      // chunk 0 at the cursor's (cell, within); chunk 1 four words later
+      int cw = within, cy = dy, cx = dx;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (j) {
+          cw += 4;
+          while (cw >= g.spw) {
+            cw -= g.spw;
+            if (++cx == g.kw) cx = 0, ++cy;
+          }
+        }
+        const int iy = iy0 + cy, ix = ix0 + cx;
+        ok[j] = mok && cy < g.kh && iy >= 0 && iy < g.H && ix >= 0 && ix < g.W;
+        if (ok[j]) x[j] = __ldg(reinterpret_cast<const uint4*>(base + ((int64_t)iy * g.W + ix) * g.sstride + cw));
+      }
+    }
+  }
+
   // A_BYTES: bytes [128 kb + 64 half, +64) of the row (awords = valid words; WS == 4)
   __device__ __forceinline__ void fetch_bytes(const Args& g, int half, uint4 (&x)[4]) {
     const int w0 = kb * 32 + 16 * half;
@@ -471,11 +518,15 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   constexpr int WPH = WS / HALVES;    // K words per producer thread per stage
   constexpr int A_STAGE_COLS = BKS / 4;
   constexpr int EPI0 = 4 + NPW;       // first epilogue warp
-  static_assert(WPH == 2 || WPH == 4, "producer word split");
+  static_assert(WPH == 2 || WPH == 4 || WPH == 8, "producer word split");
   constexpr bool POOLED = (EM == E_POOLPACK);
   constexpr int B_STAGE_BYTES = BN * BKS;
-  constexpr int SA = a_stages<BN, AM, BKS>();
-  constexpr int SB = b_stages<BN, BKS>();
+  // one ring: stage s = B tile in shared memory + A block in TMEM, one
+  // full barrier (TMA bytes + producer warps) and one empty barrier (MMA
+  // commit): the issuing thread's per-stage waits and commits are serial
+  // time the tensor pipe cannot hide at N = 128 (tools/microbench/mma_loop.cu)
+  constexpr int SA = a_stages<BN, AM, BKS>() < b_stages<BN, BKS>() ? a_stages<BN, AM, BKS>() : b_stages<BN, BKS>();
+  constexpr int SB = SA;
   constexpr int ACC_COLS = BN;
   constexpr int ACC_BUFS = acc_bufs<BN, AM>();
   constexpr int A_COL0 = ACC_BUFS * ACC_COLS;
@@ -489,9 +540,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   uint8_t* sb = smem;                                                      // SB x B_STAGE_BYTES
   int4* sthr = reinterpret_cast<int4*>(smem + SB * B_STAGE_BYTES);         // THR_COLS/2 x (mul, add, mul, add)
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + THR_COLS / 2);        // THR_COLS/32 ge-direction masks
-  uint64_t* bfull = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
-  uint64_t* bempty = bfull + SB;
-  uint64_t* full = bempty + SB;  // A ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
   uint64_t* empty = full + SA;
   uint64_t* tfull = empty + SA;
   uint64_t* tempty = tfull + ACC_BUFS;
@@ -503,12 +552,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   const int64_t tiles = mtiles * ntiles;  // tile t -> (m tile t % mtiles, n tile t / mtiles)
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < SB; ++s) {
-      mbar_init(&bfull[s], 1);  // the TMA expect_tx arrival
-      mbar_init(&bempty[s], 1);
-    }
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&full[s], NPW);  // every A-producer warp arrives
+      mbar_init(&full[s], NPW + 1);  // every A-producer warp + the TMA expect_tx arrival
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < ACC_BUFS; ++a) {
@@ -540,11 +585,11 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         const int n0 = (int)(t / mtiles) * BN;
         if constexpr (AM == A_CONV || AM == A_ROWS) prefetch_tile_inputs<AM>(g, t + 2 * (int64_t)gridDim.x, mtiles, tiles);
         for (int kb = 0; kb < g.nkb; ++kb) {
-          mbar_wait(&bempty[s], ph ^ 1);
-          mbar_expect_tx(&bfull[s], B_STAGE_BYTES);
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], B_STAGE_BYTES);
 #pragma unroll
           for (int at = 0; at < BKS / BK; ++at)  // one 128-byte-wide box per swizzle atom
-            tma_load_2d(sb + s * B_STAGE_BYTES + at * BN * BK, &bmap, &bfull[s], kb * BKS + at * BK, n0);
+            tma_load_2d(sb + s * B_STAGE_BYTES + at * BN * BK, &bmap, &full[s], kb * BKS + at * BK, n0);
           if (++s == SB) s = 0, ph ^= 1;
         }
       }
@@ -552,8 +597,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      int s = 0, sb_ = 0;
-      uint32_t ph = 0, bph = 0;
+      int s = 0;
+      uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -561,20 +606,17 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
         for (int kb = 0; kb < g.nkb; ++kb) {
-          mbar_wait(&bfull[sb_], bph);
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
-          const uint32_t bs = smem_u32(sb + sb_ * B_STAGE_BYTES);
+          const uint32_t bs = smem_u32(sb + s * B_STAGE_BYTES);
           const int kmma = kb + 1 == g.nkb ? g.klast : BKS / 32;
 #pragma unroll
           for (int k = 0; k < BKS / 32; ++k)
             if (k < kmma)
               tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, (kb | k) ? 1u : 0u);
-          tc_commit(&bempty[sb_]);
           tc_commit(&empty[s]);
           if (++s == SA) s = 0, ph ^= 1;
-          if (++sb_ == SB) sb_ = 0, bph ^= 1;
         }
         tc_commit(&tfull[acc]);
         if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
@@ -597,7 +639,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     const int64_t jobs = my_tiles * g.nkb;
     int s = 0, pending = -1;
     uint32_t ph = 0;
-    auto publish = [&](int stage, uint32_t (&v)[8 * WPH]) {
+    // every stage feeds exactly one K=32 MMA (K <= 32, one stage): the first
+    // conv; only the first word of each producer's share is consumed
+    const bool short_k = HALVES == 1 && g.nkb == 1 && g.klast == 1;
+    auto publish = [&](int stage, uint32_t (&v)[8 * WPH]) {  // WPH 2/4/8 -> 16/32/64 TMEM columns
       if (pending >= 0) {
         tmem_wait_st();
         tc_fence_before();
@@ -607,10 +652,17 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       mbar_wait(&empty[stage], ph ^ 1);
       tc_fence_after();
 #ifndef B2_PROBE_SKIP_A
-      if constexpr (WPH == 4)
-        tmem_st32(st_addr + stage * A_STAGE_COLS, v);
-      else
-        tmem_st16(st_addr + stage * A_STAGE_COLS, v);
+      if constexpr (WPH == 8) {
+        tmem_st32(st_addr + stage * A_STAGE_COLS, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_st32(st_addr + stage * A_STAGE_COLS + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      } else if constexpr (WPH == 4) {
+        if (short_k)  // one K=32 MMA reads this stage: only its 8 columns matter
+          tmem_st8(st_addr + stage * A_STAGE_COLS, v);
+        else
+          tmem_st32(st_addr + stage * A_STAGE_COLS, *reinterpret_cast<uint32_t(*)[32]>(v));
+      } else {
+        tmem_st16(st_addr + stage * A_STAGE_COLS, *reinterpret_cast<uint32_t(*)[16]>(v));
+      }
 #endif
       pending = stage;
     };
@@ -641,6 +693,39 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           }
         }
       }
+    } else if constexpr (WPH == 8) {
+      // 512-element stages: two 4-word chunks per thread, widened and stored
+      // as two 32-column TMEM writes
+      constexpr int PF8 = 2;
+      uint4 qx[PF8][2];
+      bool qok[PF8][2];
+#pragma unroll
+      for (int u = 0; u < PF8; ++u) {
+        cur.fetch_bits8(g, half, qx[u], qok[u]);
+        cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+      }
+      const int ijobs = (int)jobs;
+      for (int j0 = 0; j0 < ijobs; j0 += PF8) {
+#pragma unroll
+        for (int u = 0; u < PF8; ++u) {
+          if (j0 + u < ijobs) {
+            uint32_t v[64];
+#ifndef B2_PROBE_SKIP_A
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              widen32(qx[u][c].x, qok[u][c], v + 32 * c + 0);
+              widen32(qx[u][c].y, qok[u][c], v + 32 * c + 8);
+              widen32(qx[u][c].z, qok[u][c], v + 32 * c + 16);
+              widen32(qx[u][c].w, qok[u][c], v + 32 * c + 24);
+            }
+#endif
+            cur.fetch_bits8(g, half, qx[u], qok[u]);
+            cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+            publish(s, v);
+            if (++s == SA) s = 0, ph ^= 1;
+          }
+        }
+      }
     } else {
       // BYTECONV keeps a per-bit validity word per slot; the row and conv
       // modes only a flag (valid rows widen to +/-1, invalid ones to 0)
@@ -664,10 +749,12 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #ifndef B2_PROBE_SKIP_A
             if constexpr (MASKED) {
               widen32m(qx[u].x, qv[u].x, v + 0);
-              widen32m(qx[u].y, qv[u].y, v + 8);
-              if constexpr (WPH == 4) {
-                widen32m(qx[u].z, qv[u].z, v + 16);
-                widen32m(qx[u].w, qv[u].w, v + 24);
+              if (!short_k) {
+                widen32m(qx[u].y, qv[u].y, v + 8);
+                if constexpr (WPH == 4) {
+                  widen32m(qx[u].z, qv[u].z, v + 16);
+                  widen32m(qx[u].w, qv[u].w, v + 24);
+                }
               }
             } else {
               widen32(qx[u].x, qok[u], v + 0);
@@ -823,7 +910,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 template <int BN, int AM, int BKS>
 constexpr int smem_bytes() {
   return b_stages<BN, BKS>() * BN * BKS + THR_COLS * 8 + THR_COLS / 8 +
-         8 * (2 * b_stages<BN, BKS>() + 2 * a_stages<BN, AM, BKS>() + 6) + 16 + 1024;
+         8 * (2 * a_stages<BN, AM, BKS>() + 6) + 16 + 1024;
 }
 
 }  // namespace tc

@@ -331,12 +331,17 @@ class _Dense(_Stage):
         super().__init__(src)
         self.rec = rec
         self.w = _dev.upload(rec.words)
+        self.w8 = _dev.widen_i8(self.w, rec.units, rec.input_len) if _lib.ENGINE == "tc" else None
 
     def per_image(self):
         return (self.rec.units,)
 
     def launch(self, net, batch, st):
         r = self.rec
+        if self.w8 is not None and batch >= TC_MIN_ROWS:
+            _lib.call("b2_tc_bgemm", self.src_ptr(net), batch, _dev.P(self.w8), r.units, _wpl(r.input_len),
+                      r.input_len, _dev.P(self.out), st)
+            return
         _lib.call("b2_bgemv", _dev.P(self.w), r.units, _wpl(r.input_len), self.src_ptr(net), batch, r.input_len,
                   _dev.P(self.out), st)
 
@@ -389,6 +394,7 @@ class Network:
         self.stages = self._plan(ops)
         self.cap = 0
         self._graphs = {}
+        self._copy_stream = None
         self._reserve(max(1, int(max_batch)))
         self._scores1 = None
 
@@ -600,6 +606,10 @@ class Network:
         self._out_host = torch.empty((cap, self.classes), dtype=torch.float64, pin_memory=True)
         self._in_host_np = self._in_host.numpy()
         self._out_host_np = self._out_host.numpy()
+        # H2D staging for the pipelined host path (forward_host), allocated
+        # with the workspace so a forward pass allocates nothing
+        self._copy_stream = torch.cuda.Stream()
+        self._staged = [torch.empty_like(self._in), torch.empty_like(self._in)]
         self.cap = cap
         self._scores1 = None
 
@@ -649,20 +659,89 @@ class Network:
         g.replay()
 
     def forward_host(self, images: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
-        """(N, input_len) uint8 host images -> (N, classes) float64 scores."""
+        """(N, input_len) uint8 host images -> (N, classes) float64 scores.
+
+        Pipelined in chunks: the host copy of chunk i+1 into pinned staging
+        (multi-threaded) and its H2D copy (side stream) overlap the forward
+        pass of chunk i; each chunk's scores come back with one D2H."""
         n = images.shape[0]
         if out is None:
             out = np.empty((n, self.classes), dtype=np.float64)
-        s = torch.cuda.current_stream()
-        for b0 in range(0, n, self.cap):
-            b = min(self.cap, n - b0)
-            self._in_host_np[:b] = images[b0:b0 + b]
-            self._in[:b].copy_(self._in_host[:b], non_blocking=True)
-            self.run(b)
-            self._out_host[:b].copy_(self.scores_device[:b], non_blocking=True)
-            s.synchronize()
-            out[b0:b0 + b] = self._out_host_np[:b]
+        for s0 in range(0, n, self.cap):
+            self._forward_host_block(images[s0:s0 + self.cap], out[s0:s0 + self.cap])
         return out
+
+    def pinned_images(self, n: int) -> np.ndarray:
+        """A page-locked (n, input_len) uint8 host array: forward_batch copies
+        from it straight to the device (no staging copy on the host)."""
+        t = torch.empty((int(n), self.input_len), dtype=torch.uint8, pin_memory=True)
+        arr = t.numpy()
+        _PINNED[arr.__array_interface__["data"][0]] = t  # keep the allocation alive with the array
+        return arr
+
+    def _forward_host_block(self, images: np.ndarray, out: np.ndarray):
+        n = images.shape[0]
+        if n == 0:
+            return
+        compute = torch.cuda.current_stream()
+        src = torch.from_numpy(images) if images.flags.c_contiguous else None
+        pinned = src is not None and src.is_pinned()  # caller's page-locked memory: no host staging copy
+        ck = self.cap if self.cap < 2048 else max(1024, self.cap // 4)
+        chunks = [(b0, min(ck, n - b0)) for b0 in range(0, n, ck)]
+        half = self.cap // 2 if len(chunks) > 1 else 0  # pinned rows of slot 1
+        h2d_done = [torch.cuda.Event() for _ in chunks]   # staging buffer filled
+        consumed = [torch.cuda.Event() for _ in chunks]   # staging buffer copied into the workspace
+
+        def stage(i):
+            b0, b = chunks[i]
+            sl = i % 2
+            if pinned:
+                host = src[b0:b0 + b]
+            else:
+                if i >= 2:
+                    h2d_done[i - 2].synchronize()  # the H2D that read this pinned slot has finished
+                pin = slice(sl * half, sl * half + b)
+                _parallel_copy(self._in_host_np[pin], images[b0:b0 + b])
+                host = self._in_host[pin]
+            with torch.cuda.stream(self._copy_stream):
+                if i >= 2:
+                    self._copy_stream.wait_event(consumed[i - 2])
+                self._staged[sl][:b].copy_(host, non_blocking=True)
+                h2d_done[i].record(self._copy_stream)
+
+        stage(0)
+        for i, (b0, b) in enumerate(chunks):
+            compute.wait_event(h2d_done[i])
+            self._in[:b].copy_(self._staged[i % 2][:b], non_blocking=True)
+            consumed[i].record(compute)
+            self.run(b)
+            self._out_host[b0:b0 + b].copy_(self.scores_device[:b], non_blocking=True)
+            if i + 1 < len(chunks):
+                stage(i + 1)  # host work overlaps the forward pass just enqueued
+        compute.synchronize()
+        out[:n] = self._out_host_np[:n]
+
+
+_COPY_POOL = None
+_PINNED: dict = {}  # data pointer -> pinned torch tensor backing a pinned_images() array
+
+
+def _parallel_copy(dst: np.ndarray, src: np.ndarray, min_bytes: int = 1 << 22):
+    """dst[...] = src with several host threads for large copies (numpy
+    releases the GIL while copying)."""
+    global _COPY_POOL
+    if dst.nbytes < min_bytes:
+        np.copyto(dst, src)
+        return
+    import concurrent.futures
+    import os
+    if _COPY_POOL is None:
+        _COPY_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    parts = _COPY_POOL._max_workers
+    step = -(-dst.shape[0] // parts)
+    futs = [_COPY_POOL.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, dst.shape[0], step)]
+    for f in futs:
+        f.result()
 
 
 def _check_bn_params(r: BatchNormRecord, i: int):

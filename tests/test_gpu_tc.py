@@ -187,3 +187,28 @@ def test_network_engines_agree(networks_golden, name, monkeypatch):
         net = Network(spec, max_batch=batch.shape[0])
         got = forward_batch(net, batch)
         assert np.array_equal(got, np.concatenate([want] * reps)), engine
+
+
+def test_forward_batch_pipelined_chunks(networks_golden):
+    """forward_host pipelines chunks of cap/4 through pinned staging and two
+    device staging buffers; with N > cap it also runs several blocks.  Every
+    image must still get its own reference scores."""
+    imgs = networks_golden["bcnn_images"]
+    want = networks_golden["bcnn_scores"]
+    n = 5000
+    idx = np.arange(n) % imgs.shape[0]
+    net = Network(zoo.bcnn_spec(), max_batch=4096)
+    got = forward_batch(net, imgs[idx])
+    assert np.array_equal(got, want[idx])
+    got2 = forward_batch(net, imgs[idx[:3000]])  # one block, 3 chunks (last ragged)
+    assert np.array_equal(got2, want[idx[:3000]])
+
+
+def test_forward_batch_from_pinned_images(networks_golden):
+    imgs = networks_golden["bcnn_images"]
+    want = networks_golden["bcnn_scores"]
+    idx = np.arange(3000) % imgs.shape[0]
+    net = Network(zoo.bcnn_spec(), max_batch=2048)
+    pin = net.pinned_images(3000)
+    pin[...] = imgs[idx].reshape(3000, -1)
+    assert np.array_equal(forward_batch(net, pin), want[idx])
