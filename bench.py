@@ -319,6 +319,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         stages.append({"stage": st.name, "ms": a.elapsed_time(b) / reps, "bitops": 2 * stage_macs(st) * B})
     stage_total = sum(s["ms"] for s in stages)
+    batch1 = batch1_latency(spec, shape) if rank == 0 else None
     int8_peak, int8_src = measure_int8_peak(dev)
     for s_ in stages:
         s_["tops"] = s_["bitops"] / (s_["ms"] / 1e3) / 1e12 if s_["ms"] > 0 else 0.0
@@ -344,8 +345,29 @@ def run_ours(args, rank, world, local_rank):
                      "kernel_share_of_step": dom["ms"] / stage_total, "peak_source": int8_src,
                      "popc_pipe_peak": POPC_PEAK_TBITOPS, "popc_peak_source": POPC_PEAK_SOURCE},
         "stages": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in s_.items()} for s_ in stages],
+        "batch1": batch1,
     }
     return result
+
+
+def batch1_latency(spec, shape, reps: int = 300):
+    """The reference's own mode (network.py:506-522, forward of ONE image):
+    wall-clock microseconds per `forward(net, image)` call — host image in,
+    H2D, one CUDA-graph replay, D2H of the scores, host scores out."""
+    import torch
+    from paper_1705_07175_b200 import forward
+    from paper_1705_07175_b200.network import Network
+    net = Network(spec, max_batch=1)
+    img = np.random.default_rng(7).integers(0, 256, shape, dtype=np.uint8)
+    for _ in range(20):
+        forward(net, img)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        forward(net, img)
+    dt = (time.perf_counter() - t0) / reps
+    return {"us_per_image": round(dt * 1e6, 1), "launches_per_forward": net.launches_per_forward(),
+            "note": "wall clock per forward() call of one image, CUDA graph replay, H2D+D2H included"}
 
 
 def stage_traffic(workload, stage_name, index):
