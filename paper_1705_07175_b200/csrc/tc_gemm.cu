@@ -54,10 +54,14 @@ __device__ __forceinline__ int64_t unroll_row(int64_t img, int oy, int ox, int h
   return img * (int64_t)ho * wo + 4 * q + 2 * (oy & 1) + (ox & 1);
 }
 
-__global__ void __launch_bounds__(256) k_byte_unroll(const uint8_t* __restrict__ x, int h, int w, int c, int kh, int kw,
-                                                     int stride, int pad, int ho, int wo, int kw32, int pooled,
-                                                     const int32_t* __restrict__ t, const uint8_t* __restrict__ ge,
-                                                     uint32_t* __restrict__ out) {
+// KH/KW/C > 0: compile-time window (fully unrolled, one 32-bit word when
+// KH*KW*C <= 32); 0: runtime shape.
+template <int KH, int KW, int C>
+__global__ void __launch_bounds__(256) k_byte_unroll(const uint8_t* __restrict__ x, int h, int w, int c_, int kh_,
+                                                     int kw_, int stride, int pad, int ho, int wo, int kw32,
+                                                     int pooled, const int32_t* __restrict__ t,
+                                                     const uint8_t* __restrict__ ge, uint32_t* __restrict__ out) {
+  const int c = C ? C : c_, kh = KH ? KH : kh_, kw = KW ? KW : kw_;
   extern __shared__ uint8_t codes[];  // [in_rows][w]
   const int64_t img = blockIdx.y;
   const int oy0 = blockIdx.x * BAND;
@@ -85,6 +89,27 @@ __global__ void __launch_bounds__(256) k_byte_unroll(const uint8_t* __restrict__
   }
   __syncthreads();
   const uint32_t cmask = (1u << c) - 1u;
+  if constexpr (KH > 0 && KW > 0 && C > 0 && KH * KW * C <= 32) {
+    for (int p = threadIdx.x; p < (oy1 - oy0) * wo; p += blockDim.x) {
+      const int oy = oy0 + p / wo, ox = p - (p / wo) * wo;
+      uint32_t bits = 0, valid = 0;
+#pragma unroll
+      for (int dy = 0; dy < KH; ++dy) {
+        const int iy = oy * stride + dy - pad;
+        if (iy < 0 || iy >= h) continue;
+        const uint8_t* srow = codes + (iy - iy0) * w;
+#pragma unroll
+        for (int dx = 0; dx < KW; ++dx) {
+          const int ix = ox * stride + dx - pad;
+          if (ix < 0 || ix >= w) continue;
+          bits |= (uint32_t)srow[ix] << ((dy * KW + dx) * C);
+          valid |= cmask << ((dy * KW + dx) * C);
+        }
+      }
+      reinterpret_cast<uint2*>(out)[unroll_row(img, oy, ox, ho, wo, pooled)] = make_uint2(bits, valid);
+    }
+    return;
+  }
   for (int p = threadIdx.x; p < (oy1 - oy0) * wo; p += blockDim.x) {
     const int oy = oy0 + p / wo, ox = p % wo;
     uint32_t bits[4] = {0, 0, 0, 0}, valid[4] = {0, 0, 0, 0};
@@ -334,7 +359,8 @@ int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c
     const int in_rows = (tc::BAND - 1) * stride + kh;
     const size_t smem = (size_t)in_rows * w;
     if (smem > 48 * 1024 || batch > 65535) return B2_EINVAL;
-    tc::k_byte_unroll<<<dim3((unsigned)bands, (unsigned)batch), 256, smem, S(stream)>>>(
+    auto kern = (kh == 3 && kw == 3 && c == 3) ? tc::k_byte_unroll<3, 3, 3> : tc::k_byte_unroll<0, 0, 0>;
+    kern<<<dim3((unsigned)bands, (unsigned)batch), 256, smem, S(stream)>>>(
         x, h, w, c, kh, kw, stride, pad, g.Ho, g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
         reinterpret_cast<uint32_t*>(scratch));
   }

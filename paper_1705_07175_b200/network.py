@@ -293,10 +293,11 @@ class _BN(_Stage):
                   _thresh_struct(None, self.t64, self.ge), int(self.flat), _dev.P(self.out), st)
 
 
-# Below this many activation rows a dense layer is a weight stream (GEMV on
-# the packed weights, 8x fewer HBM bytes than int8); above it the tensor
-# cores win.
-TC_MIN_ROWS = 64
+# Dense / Input8 stages use the tensor cores from this many activation rows
+# up (measured: even at batch 1 the tcgen05 kernels beat the packed-weight
+# GEMV and the bit-plane POPC kernel, BMLP batch-1 latency 115 -> 69 us);
+# B2_TC_MIN_ROWS overrides it for comparisons.
+TC_MIN_ROWS = int(__import__("os").environ.get("B2_TC_MIN_ROWS", "1"))
 
 
 class _DenseFused(_Stage):
@@ -782,9 +783,23 @@ def forward(net: Network, image: np.ndarray) -> np.ndarray:
     next call; the same array object is returned every time."""
     x = _check_image(net, image)
     net._in_host_np[0] = x.reshape(-1)
-    net._in[:1].copy_(net._in_host[:1], non_blocking=True)
-    net.run(1)
-    net._out_host[:1].copy_(net.scores_device[:1], non_blocking=True)
+    if net.use_graphs:
+        # one graph holds H2D + the forward pass + D2H: a single launch per image
+        g = net._graphs.get("io1")
+        if g is None:
+            net.run(1)  # eager warm-up + the batch-1 compute graph
+            torch.cuda.current_stream().synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                net._in[:1].copy_(net._in_host[:1], non_blocking=True)
+                net._launch_all(1)
+                net._out_host[:1].copy_(net.scores_device[:1], non_blocking=True)
+            net._graphs["io1"] = g
+        g.replay()
+    else:
+        net._in[:1].copy_(net._in_host[:1], non_blocking=True)
+        net.run(1)
+        net._out_host[:1].copy_(net.scores_device[:1], non_blocking=True)
     torch.cuda.current_stream().synchronize()
     if net._scores1 is None:
         net._scores1 = net._out_host_np[0]
