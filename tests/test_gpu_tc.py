@@ -212,3 +212,18 @@ def test_forward_batch_from_pinned_images(networks_golden):
     pin = net.pinned_images(3000)
     pin[...] = imgs[idx].reshape(3000, -1)
     assert np.array_equal(forward_batch(net, pin), want[idx])
+
+
+def test_small_batch_cuda_core_kernels(networks_golden, monkeypatch):
+    """With the tensor-core threshold raised, dense and Input8 stages at small
+    batch run the packed-weight GEMV / bit-plane POPC kernels; they must give
+    the reference's scores too."""
+    from paper_1705_07175_b200 import forward, network
+    monkeypatch.setattr(network, "TC_MIN_ROWS", 64)
+    for name, spec in (("bmlp", zoo.bmlp_spec()), ("bcnn", zoo.bcnn_spec())):
+        imgs, want = networks_golden[f"{name}_images"][:5], networks_golden[f"{name}_scores"][:5]
+        net = Network(spec, max_batch=5)
+        assert np.array_equal(forward_batch(net, imgs), want), name
+        net1 = Network(spec, max_batch=1)
+        for i in range(2):
+            assert np.array_equal(forward(net1, imgs[i]), want[i]), (name, i)
