@@ -13,6 +13,7 @@ import os
 
 from .build import LIB
 
+LIB = os.environ.get("B2_LIB", LIB)  # A/B experiments load an alternative build
 if not os.path.exists(LIB):  # pragma: no cover - exercised on broken installs only
     raise ImportError(f"CUDA library {LIB} is missing; run `python -m paper_1705_07175_b200.build` "
                       "(this package has no CPU fallback)")

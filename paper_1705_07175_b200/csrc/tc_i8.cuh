@@ -453,9 +453,12 @@ __device__ __forceinline__ void prefetch_tile_inputs(const Args& g, int64_t t, i
 // K elements per pipeline stage (BKS): 256 for 128-column tiles (8 MMAs of
 // 64 cycles between the two ring commits — at 4 per stage the commits and
 // the issuing thread's waits cost ~40 % of the tensor pipe), else 128.
+#ifndef B2_ACC128
+#define B2_ACC128 2  // accumulator buffers of 128-column tiles (experiments: 1 buys a third A stage)
+#endif
 template <int BN, int AM>
 constexpr int acc_bufs() {
-  return BN > 128 ? 1 : (AM == A_BYTECONV ? 3 : 2);
+  return BN > 128 ? 1 : (AM == A_BYTECONV ? 3 : (B2_ACC128));
 }
 template <int BN, int AM, int BKS>
 constexpr int a_stages() {  // TMEM: accumulators + A ring fill the 512 columns
