@@ -7,6 +7,10 @@
 
 #include "tc_i8.cuh"
 
+#ifndef B2_RESIDENT_B
+#define B2_RESIDENT_B 1
+#endif
+
 namespace b2 {
 namespace tc {
 
@@ -181,6 +185,9 @@ template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4
 int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st) {
   g.nkb = (int)((k + BKS - 1) / BKS);
   g.klast = (int)(((k - 1) % BKS) / 32 + 1);
+  // one N tile whose every K stage fits the B ring space: keep it resident
+  g.resb = (g.N <= BN && (int64_t)g.nkb * BN * BKS <= (int64_t)b_stages<BN, BKS>() * BN * BKS &&
+            B2_RESIDENT_B) ? 1 : 0;
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, kpad, BN)) return rc;
   auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI>;

@@ -64,6 +64,8 @@ struct Args {
   int N;
   int nkb;    // K stages (BKS elements each)
   int klast;  // K=32 MMAs carrying data in the last stage (1..BKS/32)
+  int resb;   // the whole B tile (all K stages) stays resident in shared memory:
+              // loaded once per CTA (one N tile, nkb stages fit the ring space)
   // ---- epilogue
   int32_t* out_i32;
   int64_t ldo;
@@ -541,13 +543,15 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   // integer round trip would turn every table read into a generic load)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sb = smem;                                                      // SB x B_STAGE_BYTES
-  int4* sthr = reinterpret_cast<int4*>(smem + SB * B_STAGE_BYTES);         // THR_COLS/2 x (mul, add, mul, add)
+  // the B region is sized for b_stages() (a resident B tile may use all of it)
+  int4* sthr = reinterpret_cast<int4*>(smem + b_stages<BN, BKS>() * B_STAGE_BYTES);  // THR_COLS/2 x (mul, add, ...)
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + THR_COLS / 2);        // THR_COLS/32 ge-direction masks
   uint64_t* full = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
   uint64_t* empty = full + SA;
   uint64_t* tfull = empty + SA;
   uint64_t* tempty = tfull + ACC_BUFS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC_BUFS);
+  uint64_t* bres = tempty + ACC_BUFS;  // resident-B load complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mtiles = (g.M + BM - 1) / BM;
@@ -556,9 +560,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&full[s], NPW + 1);  // every A-producer warp + the TMA expect_tx arrival
+      mbar_init(&full[s], NPW + (g.resb ? 0 : 1));  // every A-producer warp (+ the TMA expect_tx arrival)
       mbar_init(&empty[s], 1);
     }
+    mbar_init(bres, 1);
     for (int a = 0; a < ACC_BUFS; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], NEPI);
@@ -584,9 +589,17 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         prefetch_tile_inputs<AM>(g, blockIdx.x, mtiles, tiles);
         prefetch_tile_inputs<AM>(g, blockIdx.x + gridDim.x, mtiles, tiles);
       }
+      if (g.resb) {  // one N tile: load every K stage of B once, then only prefetch A inputs
+        mbar_expect_tx(bres, (uint32_t)g.nkb * B_STAGE_BYTES);
+        for (int kb = 0; kb < g.nkb; ++kb)
+#pragma unroll
+          for (int at = 0; at < BKS / BK; ++at)
+            tma_load_2d(sb + kb * B_STAGE_BYTES + at * BN * BK, &bmap, bres, kb * BKS + at * BK, 0);
+      }
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int n0 = (int)(t / mtiles) * BN;
         if constexpr (AM == A_CONV || AM == A_ROWS) prefetch_tile_inputs<AM>(g, t + 2 * (int64_t)gridDim.x, mtiles, tiles);
+        if (g.resb) continue;
         for (int kb = 0; kb < g.nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], B_STAGE_BYTES);
@@ -604,6 +617,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
+      if (g.resb) mbar_wait(bres, 0);
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
@@ -612,7 +626,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
-          const uint32_t bs = smem_u32(sb + s * B_STAGE_BYTES);
+          const uint32_t bs = smem_u32(sb + (g.resb ? kb : s) * B_STAGE_BYTES);
           const int kmma = kb + 1 == g.nkb ? g.klast : BKS / 32;
 #pragma unroll
           for (int k = 0; k < BKS / 32; ++k)
@@ -913,7 +927,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 template <int BN, int AM, int BKS>
 constexpr int smem_bytes() {
   return b_stages<BN, BKS>() * BN * BKS + THR_COLS * 8 + THR_COLS / 8 +
-         8 * (2 * a_stages<BN, AM, BKS>() + 6) + 16 + 1024;
+         8 * (2 * a_stages<BN, AM, BKS>() + 7) + 16 + 1024;
 }
 
 }  // namespace tc
