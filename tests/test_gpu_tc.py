@@ -227,3 +227,26 @@ def test_small_batch_cuda_core_kernels(networks_golden, monkeypatch):
         net1 = Network(spec, max_batch=1)
         for i in range(2):
             assert np.array_equal(forward(net1, imgs[i]), want[i]), (name, i)
+
+
+# our fused device stage -> the reference stage whose output it reproduces
+# (tests/golden/make_golden.py records every reference stage of image 0)
+STAGE_REF = {"bcnn": {0: 2, 1: 5, 2: 7, 3: 10, 4: 12, 5: 15, 6: 17, 7: 19, 8: 20, 9: 21},
+             "bmlp": {0: 1, 1: 3, 2: 5, 3: 6, 4: 7}}
+
+
+@pytest.mark.parametrize("name", ["bcnn", "bmlp"])
+@pytest.mark.parametrize("batch", [1, 24, 300])
+def test_stage_intermediates_match_reference(networks_golden, name, batch):
+    """Every fused device stage's output for image 0 equals the reference's
+    intermediate (packed words, int32 accumulators, float64 scores)."""
+    spec = zoo.bcnn_spec() if name == "bcnn" else zoo.bmlp_spec()
+    imgs = networks_golden[f"{name}_images"]
+    net = Network(spec, max_batch=batch, use_graphs=False)
+    forward_batch(net, imgs[np.arange(batch) % imgs.shape[0]])
+    for i, st in enumerate(net.stages):
+        got = st.out[0].detach().cpu().numpy()
+        want = networks_golden[f"{name}_stage{STAGE_REF[name][i]}"]
+        if got.dtype == np.int64 and want.dtype == np.uint64:
+            got = got.view(np.uint64)
+        assert np.array_equal(got.reshape(-1), want.reshape(-1).astype(got.dtype)), (name, batch, i, st.name)
