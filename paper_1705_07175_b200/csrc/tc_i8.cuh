@@ -249,7 +249,7 @@ __device__ __forceinline__ void widen32m(uint32_t x, uint32_t valid, uint32_t* o
 // 128-element K block): walks this CTA's (tile, K block) sequence.
 //   A_ROWS / A_CONV / A_BYTECONV: 64 packed bits (uint2) + validity
 //   A_BYTES:                      64 raw bytes (4 x uint4)
-template <int AM, bool POOLED, int WS>  // WS = K words (32 elements) per stage
+template <int AM, bool POOLED, int WS, int TW>  // WS = K words per stage, TW = words per producer thread
 struct ACursor {
   int64_t t;       // tile of the next fetch
   int kb;          // K block of the next fetch
@@ -271,7 +271,7 @@ struct ACursor {
       ix0 = ox * g.stride - g.pad;
       base = g.a + img * (int64_t)g.H * g.W * g.sstride;
       cell = dy = dx = 0;
-      within = (WS / 2) * half;  // two producer warps per lane quarter
+      within = TW * half;  // this producer warp's first word of each stage
       while (within >= g.spw) within -= g.spw, step_cell(g);
     } else {
       base = g.a + (mok ? m : 0) * g.lda;
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     const int half = HALVES == 1 ? 0 : (warp - 4) >> 2;
     const int r = q * 32 + lane;  // tile row = TMEM lane
     const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / HALVES);
-    ACursor<AM, POOLED, WS> cur;
+    ACursor<AM, POOLED, WS, WPH> cur;
     cur.start(g, blockIdx.x, mtiles, tiles, r, half);
     const int64_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int64_t jobs = my_tiles * g.nkb;
