@@ -242,8 +242,9 @@ def run_ours(args, rank, world, local_rank):
     from paper_1705_07175_b200 import _lib, forward_batch, zoo
     from paper_1705_07175_b200.network import Network
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = local_rank % torch.cuda.device_count()  # == local_rank on a real N-GPU run
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     spec, shape = build_workload(args.workload)
     B = args.batch
     net = Network(spec, max_batch=B)
@@ -261,7 +262,7 @@ def run_ours(args, rank, world, local_rank):
 
     launches0 = _lib.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(gpu) as clk:
         # warm-up (also captures the CUDA graph for batch B)
         for _ in range(max(args.warmup, 1)):
             net.run(B)
@@ -277,10 +278,7 @@ def run_ours(args, rank, world, local_rank):
         clk.mark(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, world, dev)
     launches_direct = _lib.launch_count() - launches0
     gpu_launches = net.launches_per_forward() * args.steps + launches_direct
     value = args.steps * B * world / (total_ms / 1e3)
@@ -299,10 +297,7 @@ def run_ours(args, rank, world, local_rank):
         e2e_ev.append((a, b))
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
-    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e2e_ms, world, dev)
     e2e_value = args.steps * B * world / (e2e_ms / 1e3)
 
     # per-stage device time (eager launches on this stream, events)
@@ -385,6 +380,19 @@ def stage_traffic(workload, stage_name, index):
     return None
 
 
+def max_over_ranks(x: float, world: int, dev) -> float:
+    """MAX of a per-rank device time over all ranks (NCCL on the GPU; CPU
+    tensors when the process group is gloo)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return x
+    on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _dev_stream():
     from paper_1705_07175_b200 import _dev
     return _dev.stream()
@@ -431,8 +439,13 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        gpu = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        backend = os.environ.get("B2_DIST_BACKEND", "nccl")  # gloo: validate N ranks on fewer GPUs
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu:

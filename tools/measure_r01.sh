@@ -1,8 +1,10 @@
+# Round-1 measurement set (run on the GPU box from the repo root); outputs in gpurun_out/m_*
 set -x
 timeout 300 python -m pytest tests -q -m gpu --timeout 300 > gpurun_out/m_pytest.txt 2>&1
-python bench.py --cpu-seconds 10 > gpurun_out/m_bench_bcnn.json 2> gpurun_out/m_bench_bcnn.err
-python bench.py --workload bmlp --cpu-seconds 10 > gpurun_out/m_bench_bmlp.json 2> gpurun_out/m_bench_bmlp.err
+python bench.py > gpurun_out/m_bench_bcnn.json 2> gpurun_out/m_bench_bcnn.err
+python bench.py --workload bmlp > gpurun_out/m_bench_bmlp.json 2> gpurun_out/m_bench_bmlp.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/m_ref_bcnn.json 2>&1
+B2_ENGINE=popc python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/m_bench_bcnn_popc.json 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/m_launches_bcnn.csv python bench.py --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/m_launches_bmlp.csv python bench.py --workload bmlp --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
 for w in bcnn bmlp; do
@@ -10,4 +12,6 @@ for w in bcnn bmlp; do
   timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/m_traffic_$w.csv python tools/profile_stage.py --workload $w --batch $b --map gpurun_out/m_stage_map_$w.json > /dev/null 2>&1
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm -s 9 -c 1 -o gpurun_out/m_conv2_full python tools/profile_stage.py --stage 1 --reps 1 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm -s 11 -c 1 -o gpurun_out/m_conv4_full python tools/profile_stage.py --stage 3 --reps 1 > /dev/null 2>&1
+timeout 900 python tools/sweep.py > gpurun_out/m_sweeps.jsonl 2> gpurun_out/m_sweeps.err
 ls gpurun_out
