@@ -10,8 +10,11 @@
 #ifndef B2_RESIDENT_B
 #define B2_RESIDENT_B 1
 #endif
-#ifndef B2_NPW128  // producer warps of 128-column, 512-element-stage tiles
+#ifndef B2_NPW128  // producer warps of 128-column tiles
 #define B2_NPW128 8
+#endif
+#ifndef B2_BKS128  // K elements per stage of 128-column tiles
+#define B2_BKS128 512
 #endif
 
 namespace b2 {
@@ -223,7 +226,7 @@ int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k)
     return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
   } else {
     if (AM == A_CONV && g.spw % 4 != 0) return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
-    return launch_bn<128, AM, EM, B2_NPW128, 512>(g, b_i8, kpad, k, st);
+    return launch_bn<128, AM, EM, B2_NPW128, B2_BKS128>(g, b_i8, kpad, k, st);
   }
 }
 
