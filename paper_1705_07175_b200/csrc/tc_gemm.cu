@@ -16,6 +16,9 @@
 #ifndef B2_BKS128  // K elements per stage of 128-column tiles
 #define B2_BKS128 512
 #endif
+#ifndef B2_NEPI_BYTECONV  // epilogue warps of the first conv (one K block per tile)
+#define B2_NEPI_BYTECONV 8
+#endif
 
 namespace b2 {
 namespace tc {
@@ -221,7 +224,7 @@ int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k)
   if (g.M == 0 || g.N == 0) return 0;
   if (g.N > 128) return launch_bn<256, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
   if constexpr (AM == A_BYTECONV) {
-    return launch_bn<128, AM, EM, 4, 128, 8>(g, b_i8, kpad, k, st);
+    return launch_bn<128, AM, EM, 4, 128, B2_NEPI_BYTECONV>(g, b_i8, kpad, k, st);
   } else if constexpr (AM == A_BYTES) {
     return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
   } else {

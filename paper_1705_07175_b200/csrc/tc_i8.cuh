@@ -901,15 +901,28 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         if (writer) {
           const int w0 = (n0 + ec0) / 32;
           uint32_t* o = g.out_bits + site * g.ldo32 + w0;
-          if (w0 + ECH <= g.ldo32 && (g.ldo32 & 3) == 0) {
+          // vector stores sized to this warp's words (w0 is a multiple of ECH;
+          // ldo32 is always even: lines are whole uint64 words)
+          if constexpr (ECH % 4 == 0) {
+            if (w0 + ECH <= g.ldo32 && (g.ldo32 & 3) == 0) {
 #pragma unroll
-            for (int c = 0; c < ECH; c += 4)
-              *reinterpret_cast<uint4*>(o + c) = make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
-          } else {
+              for (int c = 0; c < ECH; c += 4)
+                *reinterpret_cast<uint4*>(o + c) = make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
+              goto stored;
+            }
+          } else if constexpr (ECH % 2 == 0) {
+            if (w0 + ECH <= g.ldo32) {
+#pragma unroll
+              for (int c = 0; c < ECH; c += 2) *reinterpret_cast<uint2*>(o + c) = make_uint2(words[c], words[c + 1]);
+              goto stored;
+            }
+          }
+          {
 #pragma unroll
             for (int c = 0; c < ECH; ++c)
               if (w0 + c < g.ldo32) o[c] = words[c];
           }
+        stored:;
         }
       }
       if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
