@@ -76,8 +76,9 @@ __global__ void __launch_bounds__(256) k_byte_unroll(const uint8_t* __restrict__
                                                      const uint8_t* __restrict__ ge, uint32_t* __restrict__ out) {
   const int c = C ? C : c_, kh = KH ? KH : kh_, kw = KW ? KW : kw_;
   extern __shared__ uint8_t codes[];  // [in_rows][w]
-  const int64_t img = blockIdx.y;
-  const int oy0 = blockIdx.x * BAND;
+  const int bands = (ho + BAND - 1) / BAND;  // grid = images x bands, flattened (no 65535 cap)
+  const int64_t img = blockIdx.x / bands;
+  const int oy0 = (int)(blockIdx.x % bands) * BAND;
   const int oy1 = min(oy0 + BAND, ho);
   const int iy0 = oy0 * stride - pad;
   const int in_rows = (oy1 - 1 - oy0) * stride + kh;
@@ -374,9 +375,9 @@ int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c
     const int bands = (g.Ho + tc::BAND - 1) / tc::BAND;
     const int in_rows = (tc::BAND - 1) * stride + kh;
     const size_t smem = (size_t)in_rows * w;
-    if (smem > 48 * 1024 || batch > 65535) return B2_EINVAL;
+    if (smem > 48 * 1024 || batch * bands > INT32_MAX) return B2_EINVAL;
     auto kern = (kh == 3 && kw == 3 && c == 3) ? tc::k_byte_unroll<3, 3, 3> : tc::k_byte_unroll<0, 0, 0>;
-    kern<<<dim3((unsigned)bands, (unsigned)batch), 256, smem, S(stream)>>>(
+    kern<<<(unsigned)(batch * bands), 256, smem, S(stream)>>>(
         x, h, w, c, kh, kw, stride, pad, g.Ho, g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
         reinterpret_cast<uint32_t*>(scratch));
   }

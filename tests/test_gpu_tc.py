@@ -250,3 +250,15 @@ def test_stage_intermediates_match_reference(networks_golden, name, batch):
         if got.dtype == np.int64 and want.dtype == np.uint64:
             got = got.view(np.uint64)
         assert np.array_equal(got.reshape(-1), want.reshape(-1).astype(got.dtype)), (name, batch, i, st.name)
+
+
+def test_bcnn_batch_65536(networks_golden):
+    """BASELINE configs[4]'s whole batch on one GPU (the 8-GPU run gives each
+    rank 8192 of these): every one of the 65536 images gets its reference scores."""
+    imgs, want = networks_golden["bcnn_images"], networks_golden["bcnn_scores"]
+    n = 65536
+    idx = np.arange(n) % imgs.shape[0]
+    net = Network(zoo.bcnn_spec(), max_batch=n)
+    pin = net.pinned_images(n)
+    pin[...] = imgs[idx].reshape(n, -1)
+    assert np.array_equal(forward_batch(net, pin), want[idx])
