@@ -404,7 +404,7 @@ def stage_macs(st) -> int:
     if isinstance(st, (nw._Input8Fused, nw._Input8Raw)):
         # tensor cores: one u8 x +/-1 MAC per byte; POPC engine: 8 bit-planes
         return st.units * st.k * (1 if getattr(st, "tc", False) else 8)
-    if isinstance(st, (nw._DenseFused, nw._Dense)):
+    if isinstance(st, (nw._DenseFused, nw._Dense, nw._DenseFinal)):
         return st.rec.units * st.rec.input_len
     if isinstance(st, (nw._ConvFused, nw._Conv, nw._ByteConvFused)):
         return st.h_out * st.w_out * st.rec.filters * st.rec.k

@@ -201,6 +201,14 @@ int b2_expand_i8(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, int pe
 int b2_tc_bgemm(const uint64_t* a, int64_t m, const int8_t* b_i8, int64_t n, int64_t wpl, int32_t k, int32_t* out,
                 void* stream);
 
+/* network.py _PackedDense -> _FinalBN: the last dense layer with the final
+ * float64 batch-norm (_kernels.py:285-295 bn_affine, three separately
+ * rounded ops, no FMA) in its epilogue: out (batch, units) float64 scores.
+ * mean/scale/beta: float64 per unit, as b2_bn_affine_f64. */
+int b2_tc_dense_affine_f64(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl,
+                           int32_t k, const double* mean, const double* scale, const double* beta, double* out,
+                           void* stream);
+
 /* network.py _PackedDense -> _PackedBN (flat), as b2_dense_bn_pack. */
 int b2_tc_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl, int32_t k,
                         b2_thresh th, uint64_t* out, void* stream);

@@ -63,6 +63,7 @@ SIGNATURES = {
     "b2_expand_i8": (cint, [vp, i64, i64, i64, cint, vp, vp]),
     "b2_tc_bgemm": (cint, [vp, i64, vp, i64, i64, i32, vp, vp]),
     "b2_tc_dense_bn_pack": (cint, [vp, i64, vp, i64, i64, i32, Thresh, vp, vp]),
+    "b2_tc_dense_affine_f64": (cint, [vp, i64, vp, i64, i64, i32, vp, vp, vp, vp, vp]),
     "b2_tc_conv_forward": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, vp, vp]),
     "b2_tc_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, vp, i64, cint, cint, cint, cint, cint, Thresh, vp, vp]),
     "b2_tc_input8_bn_pack": (cint, [vp, i64, i64, vp, i64, Thresh, vp, vp]),

@@ -298,6 +298,25 @@ int b2_tc_bgemm(const uint64_t* a, int64_t m, const int8_t* b_i8, int64_t n, int
   return tc::launch<tc::A_ROWS, tc::E_I32>(g, b_i8, tc::kpad_of(k), S(stream), k);
 }
 
+int b2_tc_dense_affine_f64(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl,
+                           int32_t k, const double* mean, const double* scale, const double* beta, double* out,
+                           void* stream) {
+  if (units < 1 || units > INT32_MAX || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl || !mean || !scale || !beta)
+    return B2_EINVAL;
+  tc::Args g{};
+  g.a = reinterpret_cast<const uint32_t*>(x);
+  g.lda = 2 * wpl;
+  g.awords = (k + 31) / 32;
+  g.M = batch;
+  g.N = (int)units;
+  g.mean = mean;
+  g.scale = scale;
+  g.beta = beta;
+  g.out_f64 = out;
+  g.ldo = units;
+  return tc::launch<tc::A_ROWS, tc::E_AFFINE>(g, w_i8, tc::kpad_of(k), S(stream), k);
+}
+
 int b2_tc_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl, int32_t k,
                         b2_thresh th, uint64_t* out, void* stream) {
   if (units < 1 || units > INT32_MAX || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl || !th.thresh || !th.ge_dir)

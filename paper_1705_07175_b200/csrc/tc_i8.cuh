@@ -50,7 +50,7 @@ constexpr int PF = 4;                   // A-producer prefetch depth (K blocks)
 // A operand sources: packed rows; implicit bit-im2col of NHWC-bits
 // activations; raw u8 rows; masked window rows of the byte-input first conv
 enum AMode { A_ROWS = 0, A_CONV = 1, A_BYTES = 2, A_BYTECONV = 3 };
-enum EMode { E_I32 = 0, E_PACK = 1, E_POOLPACK = 2 };
+enum EMode { E_I32 = 0, E_PACK = 1, E_POOLPACK = 2, E_AFFINE = 3 };
 
 struct Args {
   // ---- A operand
@@ -73,6 +73,11 @@ struct Args {
   int64_t ldo32;
   const int32_t* thresh;
   const uint8_t* ge;
+  // E_AFFINE: final float64 batch-norm of the int32 accumulators
+  const double* mean;
+  const double* scale;
+  const double* beta;
+  double* out_f64;  // (M, N), leading dimension ldo
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -816,7 +821,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     // when all N columns fit the table, else staged per tile
     const int ncols = ntiles * BN;
     const bool static_thr = ncols <= THR_COLS;
-    if constexpr (EM != E_I32) {
+    if constexpr (EM == E_PACK || EM == E_POOLPACK) {
       if (static_thr) {
         stage_thresholds(g, 0, ncols, et, 32 * NEPI, lane, sthr, sgm);
         epi_bar<NEPI>();
@@ -827,7 +832,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       const int n0 = (int)(t / mtiles) * BN;
       const int tcol = static_thr ? n0 : 0;  // table column of this tile's first column
       const bool mok = m < g.M;
-      if constexpr (EM != E_I32) {
+      if constexpr (EM == E_PACK || EM == E_POOLPACK) {
         if (!static_thr) {  // N too wide for the resident table: this tile's columns only
           epi_bar<NEPI>();
           stage_thresholds(g, n0, BN, et, 32 * NEPI, lane, sthr, sgm);
@@ -853,7 +858,20 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         uint32_t(&vn)[32] = (c & 1) ? va : vb;
         if (c + 1 < ECH) tmem_ld32(tmem + lane_addr + acc * ACC_COLS + (c + 1) * 32, vn);
         const int nb = n0 + ec0 + c * 32;
-        if constexpr (EM == E_I32) {
+        if constexpr (EM == E_AFFINE) {
+          // _kernels.py:285-295 bn_affine: three separately rounded IEEE
+          // operations (no FMA contraction), bit-exact with numpy
+          if (mok && nb < g.N) {
+            double* o = g.out_f64 + m * g.ldo + nb;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = nb + j;
+              if (n < g.N)
+                o[j] = __dadd_rn(__dmul_rn(__dsub_rn((double)(int)v[j], __ldg(g.mean + n)), __ldg(g.scale + n)),
+                                 __ldg(g.beta + n));
+            }
+          }
+        } else if constexpr (EM == E_I32) {
           if (mok && nb < g.N) {
             int32_t* o = g.out_i32 + m * g.ldo + nb;
             if (nb + 32 <= g.N && ((g.ldo & 3) == 0)) {
@@ -895,7 +913,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if constexpr (EM != E_I32) {
+      if constexpr (EM == E_PACK || EM == E_POOLPACK) {
         const int64_t site = POOLED ? (m >> 2) : m;
         const bool writer = mok && (!POOLED || (lane & 3) == 0);
         if (writer) {

@@ -347,6 +347,41 @@ class _Dense(_Stage):
                   _dev.P(self.out), st)
 
 
+class _DenseFinal(_Stage):
+    """_PackedDense -> _FinalBN in one tensor-core launch (network.py:153-162,
+    259-270): int32 dot products, then float64 scores in the epilogue."""
+
+    name = "dense+final-bn"
+    out_dtype = np.float64
+
+    def __init__(self, src, rec, bn_dev, dense: "_Dense"):
+        super().__init__(src)
+        self.rec, self.bn = rec, bn_dev
+        self.dense = dense  # the unfused pair, for batches below TC_MIN_ROWS
+        self.final = _FinalBN(dense, bn_dev, rec.units, XKIND[np.dtype(np.int32)])
+
+    def per_image(self):
+        return (self.rec.units,)
+
+    def alloc(self, cap):
+        super().alloc(cap)
+        self.dense.alloc(cap)
+        self.final.out = self.out
+
+    def launches(self):
+        return 1
+
+    def launch(self, net, batch, st):
+        r = self.rec
+        if batch < TC_MIN_ROWS:
+            self.dense.launch(net, batch, st)
+            self.final.launch(net, batch, st)
+            return
+        _lib.call("b2_tc_dense_affine_f64", self.src_ptr(net), batch, _dev.P(self.dense.w8), r.units,
+                  _wpl(r.input_len), r.input_len, _dev.P(self.bn["mean64"]), _dev.P(self.bn["scale64"]),
+                  _dev.P(self.bn["beta64"]), _dev.P(self.out), st)
+
+
 class _FinalBN(_Stage):
     name = "final-bn"
     out_dtype = np.float64
@@ -576,6 +611,11 @@ class Network:
                 if nxt["kind"] == "bn":
                     st = _DenseFused(src, r, cal(nxt, r.input_len))
                     j += 2
+                elif nxt["kind"] == "final" and _lib.ENGINE == "tc":
+                    dense = _Dense(src, r)
+                    st = _DenseFinal(src, r, cal(nxt, 0), dense)
+                    dense.src = src
+                    j += 2
                 else:
                     st = _Dense(src, r)
                     j += 1
@@ -675,10 +715,8 @@ class Network:
     def pinned_images(self, n: int) -> np.ndarray:
         """A page-locked (n, input_len) uint8 host array: forward_batch copies
         from it straight to the device (no staging copy on the host)."""
-        t = torch.empty((int(n), self.input_len), dtype=torch.uint8, pin_memory=True)
-        arr = t.numpy()
-        _PINNED[arr.__array_interface__["data"][0]] = t  # keep the allocation alive with the array
-        return arr
+        # the array's base keeps the pinned tensor (and its allocation) alive
+        return torch.empty((int(n), self.input_len), dtype=torch.uint8, pin_memory=True).numpy()
 
     def _forward_host_block(self, images: np.ndarray, out: np.ndarray):
         n = images.shape[0]
@@ -724,7 +762,6 @@ class Network:
 
 
 _COPY_POOL = None
-_PINNED: dict = {}  # data pointer -> pinned torch tensor backing a pinned_images() array
 
 
 def _parallel_copy(dst: np.ndarray, src: np.ndarray, min_bytes: int = 1 << 22):

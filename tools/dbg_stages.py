@@ -7,7 +7,7 @@ from paper_1705_07175_b200 import zoo, _dev, forward_batch
 from paper_1705_07175_b200.network import Network
 g = np.load(__import__("os").path.join(sys.path[0], "tests", "golden", "networks.npz"))
 imgs = g["bcnn_images"]
-ref_of = {0: 2, 1: 5, 2: 7, 3: 10, 4: 12, 5: 15, 6: 17, 7: 19, 8: 20, 9: 21}
+ref_of = {0: 2, 1: 5, 2: 7, 3: 10, 4: 12, 5: 15, 6: 17, 7: 19, 8: 21}  # 8 = dense + final batch-norm
 for B in (1, 24, 300):
     net = Network(zoo.bcnn_spec(), max_batch=B, use_graphs=False)
     x = imgs[np.arange(B) % 24]
