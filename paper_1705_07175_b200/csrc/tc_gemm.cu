@@ -16,6 +16,9 @@
 #ifndef B2_BKS128  // K elements per stage of 128-column tiles
 #define B2_BKS128 512
 #endif
+#ifndef B2_BYTES_BN128  // Input8 (u8 rows) on 128-column tiles
+#define B2_BYTES_BN128 0
+#endif
 #ifndef B2_NEPI_BYTECONV  // epilogue warps of the first conv (one K block per tile)
 #define B2_NEPI_BYTECONV 8
 #endif
@@ -223,6 +226,11 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
 template <int AM, int EM>
 int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k) {
   if (g.M == 0 || g.N == 0) return 0;
+#if B2_BYTES_BN128
+  // u8 rows need no widening: re-reading A per 128-column tile is cheap and
+  // buys the double-buffered accumulator
+  if constexpr (AM == A_BYTES) return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
+#endif
   if (g.N > 128) return launch_bn<256, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
   if constexpr (AM == A_BYTECONV) {
     return launch_bn<128, AM, EM, 4, 128, B2_NEPI_BYTECONV>(g, b_i8, kpad, k, st);
