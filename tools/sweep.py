@@ -6,6 +6,9 @@
   (_kernels.py:85-106 bgemm_packed semantics) through gemm.bgemm_device on
   device-resident packed operands (B widened once, outside the timing, like
   a layer's weights); both engines.
+* sign-pack (_kernels.py:43-54, float32 -> bits) and byte bit-planes
+  (_kernels.py:67-82): HBM-bound, reported in GB/s of algorithmic bytes
+  (input + output) against MEASURED_PEAKS.json's copy bandwidth.
 * binary conv 3x3 / stride 1 / pad 1, C_in = C_out in {128, 256, 512, 1024},
   H = W in {8, 16, 32, 64}, batch 256, fused batchnorm-threshold + repack
   output (b2_tc_conv_bn_pack), i.e. a network conv stage.
@@ -85,6 +88,33 @@ def conv_case(c, hw, batch, flush, reps):
             "Tops": round(ops / (ms / 1e3) / 1e12, 1), "images_per_s": round(batch / (ms / 1e3))}
 
 
+def pack_case(kind, flush, reps):
+    rng = np.random.default_rng(3)
+    if kind == "sign_pack_f32":
+        lines, bits = 262144, 4096  # 4 GiB of float32 in, 128 MiB of words out
+        x = torch.randn((lines, bits), dtype=torch.float32, device="cuda")
+        out = _dev.empty((lines, bits // 64), np.uint64)
+        fn = lambda: _lib.call("b2_pack_lines_f32", _dev.P(x), lines, bits, _dev.P(out), _dev.stream())  # noqa: E731
+        nbytes = lines * bits * 4 + lines * bits // 8
+        ref_in = x[:4].cpu().numpy()
+        fn()
+        got = _dev.download(out[:4], np.uint64)
+        want = zoo.pack_bits_host(~(ref_in < 0))
+        assert np.array_equal(got, want)
+    else:
+        lines, bits = 1048576, 784  # MNIST-shaped bytes -> 8 bit-planes
+        x = torch.from_numpy(rng.integers(0, 256, (lines, bits), dtype=np.uint8)).cuda()
+        out = _dev.empty((8, lines, -(-bits // 64)), np.uint64)
+        fn = lambda: _lib.call("b2_pack_byte_planes", _dev.P(x), lines, bits, _dev.P(out), _dev.stream())  # noqa: E731
+        nbytes = lines * bits + 8 * lines * (-(-bits // 64)) * 8
+    ms = timed(fn, reps, flush)
+    import json as _j
+    peak = _j.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    gbs = nbytes / (ms / 1e3) / 1e9
+    return {"case": kind, "lines": lines, "bits": bits, "ms": round(ms, 4), "GBps": round(gbs, 1),
+            "frac_of_hbm": round(gbs / peak, 3), "hbm_peak_GBps": peak}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
@@ -97,6 +127,8 @@ def main():
             if engine == "popc" and n > 8192:
                 continue
             print(json.dumps(bgemm_case(n, engine, flush, 3 if n >= 8192 else 10)), flush=True)
+    for kind in ("sign_pack_f32", "byte_planes"):
+        print(json.dumps(pack_case(kind, flush, 5)), flush=True)
     for c in (128, 256, 512, 1024):
         for hw in (8, 16, 32, 64):
             if a.quick and (c, hw) not in ((128, 32), (512, 8)):
