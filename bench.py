@@ -315,6 +315,7 @@ def run_ours(args, rank, world, local_rank):
         stages.append({"stage": st.name, "ms": a.elapsed_time(b) / reps, "bitops": 2 * stage_macs(st) * B})
     stage_total = sum(s["ms"] for s in stages)
     batch1 = batch1_latency(spec, shape) if rank == 0 else None
+    others = other_metrics(args, dev, flush) if rank == 0 and not args.no_extra else None
     int8_peak, int8_src = measure_int8_peak(dev)
     for s_ in stages:
         s_["tops"] = s_["bitops"] / (s_["ms"] / 1e3) / 1e12 if s_["ms"] > 0 else 0.0
@@ -341,8 +342,59 @@ def run_ours(args, rank, world, local_rank):
                      "popc_pipe_peak": POPC_PEAK_TBITOPS, "popc_peak_source": POPC_PEAK_SOURCE},
         "stages": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in s_.items()} for s_ in stages],
         "batch1": batch1,
+        "other_metrics": others,
     }
     return result
+
+
+def other_metrics(args, dev, flush, steps: int = 10):
+    """The rest of BASELINE's metric on the same GPU, device-timed like
+    `value`: the other network (BMLP for a BCNN run and vice versa) and the
+    bit-packed GEMM at M=N=K=8192 (configs[2])."""
+    import torch
+    from paper_1705_07175_b200 import _dev, gemm, zoo
+    from paper_1705_07175_b200.network import Network
+    out = {}
+    other = "bmlp" if args.workload == "bcnn" else "bcnn"
+    spec, shape = build_workload(other)
+    b = 16384 if other == "bmlp" else 8192
+    net = Network(spec, max_batch=b)
+    net.input_device.copy_(torch.from_numpy(
+        np.random.default_rng(5).integers(0, 256, (b, int(np.prod(shape))), dtype=np.uint8)).to(dev))
+    for _ in range(3):
+        net.run(b)
+    ms = 0.0
+    for _ in range(steps):
+        flush.fill_(7)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        net.run(b)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    out[f"{other}_images_per_s"] = b * steps / (ms / 1e3)
+    out[f"{other}_batch"] = b
+    del net
+    n = 8192
+    rng = np.random.default_rng(6)
+    a = _dev.upload(zoo.pack_bits_host(rng.random((n, n)) >= 0.5))
+    w = _dev.upload(zoo.pack_bits_host(rng.random((n, n)) >= 0.5))
+    w8 = _dev.widen_i8(w, n, n)
+    c = _dev.empty((n, n), np.int32)
+    for _ in range(3):
+        gemm.bgemm_device(a, n, w, n, n // 64, n, c, b_i8=w8)
+    ms = 0.0
+    for _ in range(5):
+        flush.fill_(9)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        gemm.bgemm_device(a, n, w, n, n // 64, n, c, b_i8=w8)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    out["bgemm_8192_Gops"] = 2.0 * n ** 3 * 5 / (ms / 1e3) / 1e9
+    out["note"] = "device time, CUDA events, L2 flushed between steps; ops = 2 per binary MAC"
+    return out
 
 
 def batch1_latency(spec, shape, reps: int = 300):
@@ -422,6 +474,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other_metrics block")
     args = ap.parse_args()
     if args.batch is None:
         args.batch = 8192 if args.workload == "bcnn" else 16384

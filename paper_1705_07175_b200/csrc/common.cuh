@@ -20,6 +20,19 @@ inline int launched() {
 }
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device,
+// once per (kernel, device): the attribute is per device, and one process
+// may drive several GPUs.  `done` is the caller's per-kernel static bitmask.
+template <typename K>
+inline void smem_optin(K kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_relaxed);
+}
 inline int64_t wpl64(int64_t bits) { return (bits + 63) >> 6; }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

@@ -9,11 +9,8 @@ constexpr int TM_ = 16, TN_ = 2, WN_ = 2;
 template <int CWA, int CWB, bool CONV, int MODE>
 int launch_gemm(const GemmArgs& g, cudaStream_t st) {
   auto kern = k_popc_gemm<Cfg, CWA, CWB, CONV, MODE, TM_, TN_, WN_>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(kern, Cfg::SMEM, attr);
   if (g.M == 0 || g.N == 0) return 0;
   dim3 grid((unsigned)cdiv(g.M, Cfg::BM), (unsigned)cdiv(g.N, Cfg::BN));
   kern<<<grid, 256, Cfg::SMEM, st>>>(g);

@@ -192,11 +192,8 @@ int b2_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const uint64_t
   if (!batch) return 0;
   int pitchw = kw32 | 1;
   size_t smem = sizeof(uint32_t) * ((size_t)I8_IMG * 8 * kw32 + 32 * I8_TN * pitchw + I8_IMG);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_input8_bn_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(k_input8_bn_pack, 200 * 1024, attr);
   dim3 grid((unsigned)cdiv(batch, I8_IMG), (unsigned)cdiv(units, 32 * I8_TN));
   k_input8_bn_pack<<<grid, 256, smem, S(stream)>>>(x, batch, (int)k, kw32, (const uint32_t*)w, units, kw32,
                                                    th.thresh, th.ge_dir, (uint32_t*)out, 2 * wpl64(units));
@@ -226,11 +223,8 @@ int b2_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b
   int ldo32 = (int)(2 * wpl64(filters));
   size_t smem = sizeof(uint32_t) * ((size_t)h * w + 2 * ldo32 * 32) + ldo32 * 32;
   if (smem > 200 * 1024) return B2_EINVAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_byte_conv_bn_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(k_byte_conv_bn_pack, 200 * 1024, attr);
   int64_t ldw = 2 * wpl64((int64_t)kh * kw * c);
   k_byte_conv_bn_pack<<<(unsigned)batch, 256, smem, S(stream)>>>(x, h, w, c, th_in.thresh, th_in.ge_dir,
                                                                  (const uint32_t*)wwords, ldw, (int)filters, kh, kw,

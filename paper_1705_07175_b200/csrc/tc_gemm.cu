@@ -205,11 +205,8 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   if (int rc = make_bmap(&map, b_i8, g.N, kpad, BN)) return rc;
   auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI>;
   constexpr int smem = smem_bytes<BN, AM, BKS>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(kern, smem, attr);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
   kern<<<grid, num_threads<NPW, NEPI>(), smem, st>>>(map, g);
