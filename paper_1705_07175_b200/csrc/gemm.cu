@@ -33,37 +33,50 @@ inline int chunk_words(int64_t a, int64_t b) {
   return 1;
 }
 
-// Batch-small dense: one warp per output unit, lanes over K words
-// (coalesced weight rows), __reduce_add_sync, then (PACK) ballot of 32 units.
+// Batch-small dense (_kernels.py:109-117 bgemv_packed, batched over <= 8
+// activation lines): a weight stream.  A block of 8 warps owns 32 units;
+// each warp computes 4 of them with all their K-word loads in flight (lanes
+// stride K for coalescing), reduces with __reduce_add_sync, and the block
+// assembles the 32 results (PACK: one threshold word via ballot).
 template <bool PACK>
 __global__ void __launch_bounds__(256) k_dense_small(const uint32_t* __restrict__ x, int64_t batch, int64_t ldx,
                                                     const uint32_t* __restrict__ w, int64_t units, int64_t ldw,
                                                     int kw32, int32_t kbits, int32_t* __restrict__ out,
                                                     uint32_t* __restrict__ out_bits, int64_t ldo32,
                                                     const int32_t* __restrict__ thresh, const uint8_t* __restrict__ ge) {
-  const int lane = threadIdx.x & 31;
-  const int64_t ubase = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;  // 32 units per warp
+  __shared__ int32_t res[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ubase = (int64_t)blockIdx.x * 32;
+  const int64_t u0 = ubase + warp * 4;
   for (int64_t bi = 0; bi < batch; ++bi) {
     const uint32_t* xr = x + bi * ldx;
-    int32_t mine = 0;
-    for (int uu = 0; uu < 32; ++uu) {
-      int64_t u = ubase + uu;
-      if (u >= units) break;  // warp-uniform
-      const uint32_t* wr = w + u * ldw;
-      uint32_t part = 0;
-      for (int k = lane; k < kw32; k += 32) part += __popc(wr[k] ^ xr[k]);
-      uint32_t tot = __reduce_add_sync(0xffffffffu, part);
-      if (lane == uu) mine = kbits - 2 * (int32_t)tot;
+    uint32_t part[4] = {0, 0, 0, 0};
+#pragma unroll 4
+    for (int k = lane; k < kw32; k += 32) {
+      const uint32_t xv = __ldg(xr + k);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (u0 + i < units) part[i] += __popc(__ldg(w + (u0 + i) * ldw + k) ^ xv);
     }
-    int64_t u = ubase + lane;
-    if constexpr (PACK) {
-      bool bit = u < units && thr_bit(mine, thresh[u < units ? u : 0], ge[u < units ? u : 0] != 0);
-      uint32_t word = __ballot_sync(0xffffffffu, bit);
-      int64_t widx = ubase >> 5;
-      if (lane == 0 && widx < ldo32) out_bits[bi * ldo32 + widx] = word;
-    } else {
-      if (u < units) out[bi * units + u] = mine;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, part[i]);
+      if (lane == 0) res[warp * 4 + i] = kbits - 2 * (int32_t)tot;
     }
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t u = ubase + lane;
+      const int32_t mine = res[lane];
+      if constexpr (PACK) {
+        const bool bit = u < units && thr_bit(mine, thresh[u < units ? u : 0], ge[u < units ? u : 0] != 0);
+        const uint32_t word = __ballot_sync(0xffffffffu, bit);
+        const int64_t widx = ubase >> 5;
+        if (lane == 0 && widx < ldo32) out_bits[bi * ldo32 + widx] = word;
+      } else {
+        if (u < units) out[bi * units + u] = mine;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -177,7 +190,7 @@ int b2_bgemv(const uint64_t* w, int64_t units, int64_t wpl, const uint64_t* x, i
   if (units < 0 || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl) return B2_EINVAL;
   if (!units || !batch) return 0;
   if (batch <= 8) {
-    k_dense_small<false><<<(unsigned)cdiv(units, 256), 256, 0, S(stream)>>>(
+    k_dense_small<false><<<(unsigned)cdiv(units, 32), 256, 0, S(stream)>>>(
         (const uint32_t*)x, batch, 2 * wpl, (const uint32_t*)w, units, 2 * wpl, (int)(2 * wpl), k, out, nullptr, 0,
         nullptr, nullptr);
     return launched();
@@ -191,7 +204,7 @@ int b2_dense_bn_pack(const uint64_t* x, int64_t batch, const uint64_t* w, int64_
   if (!batch) return 0;
   int64_t ldo32 = 2 * wpl64(units);
   if (batch <= 8) {
-    k_dense_small<true><<<(unsigned)cdiv(units, 256), 256, 0, S(stream)>>>(
+    k_dense_small<true><<<(unsigned)cdiv(units, 32), 256, 0, S(stream)>>>(
         (const uint32_t*)x, batch, 2 * wpl, (const uint32_t*)w, units, 2 * wpl, (int)(2 * wpl), k, nullptr,
         (uint32_t*)out, ldo32, th.thresh, th.ge_dir);
     return launched();

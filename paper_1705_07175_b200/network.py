@@ -298,6 +298,10 @@ class _BN(_Stage):
 # GEMV and the bit-plane POPC kernel, BMLP batch-1 latency 115 -> 69 us);
 # B2_TC_MIN_ROWS overrides it for comparisons.
 TC_MIN_ROWS = int(__import__("os").environ.get("B2_TC_MIN_ROWS", "1"))
+# Dense stages below this many rows stream the packed weights on the CUDA
+# cores (k_dense_small: all of a unit's K words in flight, 8x fewer bytes
+# than the int8 tiles) instead of the tensor cores.
+TC_MIN_ROWS_DENSE = int(__import__("os").environ.get("B2_TC_MIN_ROWS_DENSE", "9"))
 
 
 class _DenseFused(_Stage):
@@ -314,7 +318,7 @@ class _DenseFused(_Stage):
 
     def launch(self, net, batch, st):
         r = self.rec
-        if self.w8 is not None and batch >= TC_MIN_ROWS:
+        if self.w8 is not None and batch >= max(TC_MIN_ROWS, TC_MIN_ROWS_DENSE):
             _lib.call("b2_tc_dense_bn_pack", self.src_ptr(net), batch, _dev.P(self.w8), r.units, _wpl(r.input_len),
                       r.input_len, _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]),
                       _dev.P(self.out), st)
@@ -339,7 +343,7 @@ class _Dense(_Stage):
 
     def launch(self, net, batch, st):
         r = self.rec
-        if self.w8 is not None and batch >= TC_MIN_ROWS:
+        if self.w8 is not None and batch >= max(TC_MIN_ROWS, TC_MIN_ROWS_DENSE):
             _lib.call("b2_tc_bgemm", self.src_ptr(net), batch, _dev.P(self.w8), r.units, _wpl(r.input_len),
                       r.input_len, _dev.P(self.out), st)
             return
@@ -373,7 +377,7 @@ class _DenseFinal(_Stage):
 
     def launch(self, net, batch, st):
         r = self.rec
-        if batch < TC_MIN_ROWS:
+        if batch < max(TC_MIN_ROWS, TC_MIN_ROWS_DENSE):
             self.dense.launch(net, batch, st)
             self.final.launch(net, batch, st)
             return
