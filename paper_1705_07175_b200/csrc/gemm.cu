@@ -204,7 +204,8 @@ int b2_dense_bn_pack(const uint64_t* x, int64_t batch, const uint64_t* w, int64_
   if (!batch) return 0;
   int64_t ldo32 = 2 * wpl64(units);
   if (batch <= 8) {
-    k_dense_small<true><<<(unsigned)cdiv(units, 32), 256, 0, S(stream)>>>(
+    // one block per output word, padding words included (they must be written as 0)
+    k_dense_small<true><<<(unsigned)(cdiv(units, 32) > ldo32 ? cdiv(units, 32) : ldo32), 256, 0, S(stream)>>>(
         (const uint32_t*)x, batch, 2 * wpl, (const uint32_t*)w, units, 2 * wpl, (int)(2 * wpl), k, nullptr,
         (uint32_t*)out, ldo32, th.thresh, th.ge_dir);
     return launched();

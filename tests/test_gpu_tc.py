@@ -264,3 +264,26 @@ def test_bcnn_batch_65536(networks_golden):
     pin = net.pinned_images(n)
     pin[...] = imgs[idx].reshape(n, -1)
     assert np.array_equal(forward_batch(net, pin), want[idx])
+
+
+@pytest.mark.parametrize("batch", [1, 3, 100])
+@pytest.mark.parametrize("units,k", [(10, 64), (200, 4608), (32, 32), (65, 100), (130, 1000)])
+def test_packed_outputs_fully_written(oracle, batch, units, k):
+    """Every kernel writes its whole `out` (include/bitnn_b200.h): packed
+    lines are padded to whole uint64 words and the padding bits must come out
+    0 even when the buffer held garbage (the next layer XORs them)."""
+    rng = np.random.default_rng(units * 7 + k + batch)
+    x = oracle.pack_lines(rand_pm1(rng, batch, k))
+    wt = oracle.pack_lines(rand_pm1(rng, units, k))
+    bn = rand_bn(rng, units, 3.0)
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, k)
+    want = oracle.threshold_sign_pack(oracle.bgemm(x, wt, k), bn.thresh, bn.ge_dir, True) if batch == 1 else \
+        np.stack([oracle.threshold_sign_pack(r.reshape(1, -1), bn.thresh, bn.ge_dir, True)[0]
+                  for r in oracle.bgemm(x, wt, k)])
+    want = want.reshape(batch, -1)
+    for name in ("b2_dense_bn_pack", "b2_tc_dense_bn_pack"):
+        out = _dev.upload(np.full((batch, -(-units // 64)), 0xFFFFFFFFFFFFFFFF, np.uint64))
+        wd = _dev.upload(wt) if name == "b2_dense_bn_pack" else _dev.widen_i8(_dev.upload(wt), units, k)
+        _lib.call(name, _dev.P(_dev.upload(x)), batch, _dev.P(wd), units, -(-k // 64), k, th(cal), _dev.P(out),
+                  _dev.stream())
+        assert np.array_equal(_dev.download(out, np.uint64), want), name
