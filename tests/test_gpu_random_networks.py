@@ -35,7 +35,7 @@ def random_cnn(rng):
     c0 = int(rng.choice([1, 3, 4]))
     k0 = int(rng.choice([3, 5])) if c0 <= 3 else 3
     recs = [bn(rng, c0, 100.0)]
-    c = int(rng.choice([64, 128]))
+    c = int(rng.choice([32, 64, 128]))  # 32: CUDA-core conv kernels even on the tensor-core engine
     recs.append(ConvRecord(c, k0, k0, 1, k0 // 2, c0, rows(rng, c, k0 * k0 * c0)))
     size = h
     for _ in range(int(rng.integers(1, 4))):
@@ -46,7 +46,7 @@ def random_cnn(rng):
             recs.append(MaxPoolRecord(3, 3, 1))  # unfused pool path
             size -= 2
         recs.append(bn(rng, c, 8.0 * np.sqrt(9 * c) / 10))
-        f = int(rng.choice([64, 128, 192, 256]))
+        f = int(rng.choice([64, 96, 128, 192, 256]))
         recs.append(ConvRecord(f, 3, 3, 1, 1, c, rows(rng, f, 9 * c)))
         c = f
     if size % 2 == 0 and rng.random() < 0.5:
@@ -68,8 +68,11 @@ def random_mlp(rng):
     return ModelSpec((1, 1, k), recs)
 
 
-@pytest.mark.parametrize("seed", range(12))
-def test_random_networks_vs_oracle(oracle, seed):
+@pytest.mark.parametrize("engine", ["tc", "popc"])
+@pytest.mark.parametrize("seed", range(16))
+def test_random_networks_vs_oracle(oracle, seed, engine, monkeypatch):
+    from paper_1705_07175_b200 import _lib
+    monkeypatch.setattr(_lib, "ENGINE", engine)
     rng = np.random.default_rng(9000 + seed)
     spec = random_cnn(rng) if seed % 3 else random_mlp(rng)
     h, w, c = spec.input_dims
