@@ -287,3 +287,51 @@ def test_packed_outputs_fully_written(oracle, batch, units, k):
         _lib.call(name, _dev.P(_dev.upload(x)), batch, _dev.P(wd), units, -(-k // 64), k, th(cal), _dev.P(out),
                   _dev.stream())
         assert np.array_equal(_dev.download(out, np.uint64), want), name
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_tc_conv_forward_random_geometry(oracle, seed):
+    rng = np.random.default_rng(4000 + seed)
+    c = int(rng.choice([64, 128, 192, 256, 320]))
+    kh, kw = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+    stride, pad = int(rng.integers(1, 4)), int(rng.integers(0, 3))
+    h = int(rng.integers(max(1, kh - 2 * pad), 21))
+    w = int(rng.integers(max(1, kw - 2 * pad), 21))
+    f, batch = int(rng.integers(1, 301)), int(rng.integers(1, 5))
+    xs = np.stack([oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)])
+    wt = oracle.pack_lines(rand_pm1(rng, f, kh * kw * c))
+    corr = oracle.compute_correction(wt, (h, w, c), (kh, kw), stride, pad)
+    ho, wo = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
+    want = np.stack([oracle.bgemm(oracle.unroll_packed(x, h, w, c, kh, kw, stride, pad), wt, kh * kw * c) + corr
+                     for x in xs]).reshape(batch, ho, wo, f)
+    w8 = _dev.widen_i8(_dev.upload(wt), f, kh * kw * c)
+    out = _dev.upload(np.full((batch, ho, wo, f), -7, np.int32))
+    _lib.call("b2_tc_conv_forward", _dev.P(_dev.upload(xs)), batch, h, w, c, _dev.P(w8), f, kh, kw, stride, pad,
+              _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.int32), want), (h, w, c, f, kh, kw, stride, pad, batch)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_tc_conv_bn_pack_random_geometry(oracle, seed):
+    rng = np.random.default_rng(5000 + seed)
+    c = int(rng.choice([64, 128, 256]))
+    pool = bool(rng.integers(0, 2))
+    h, w = 2 * int(rng.integers(1, 9)), 2 * int(rng.integers(1, 9))
+    f, batch = int(rng.integers(1, 300)), int(rng.integers(1, 4))
+    xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
+    wt = oracle.pack_lines(rand_pm1(rng, f, 9 * c))
+    bn = rand_bn(rng, f, 10.0)
+    corr = oracle.compute_correction(wt, (h, w, c), (3, 3), 1, 1)
+    want = []
+    for x in xs:
+        acc = (oracle.bgemm(oracle.unroll_packed(x, h, w, c, 3, 3, 1, 1), wt, 9 * c) + corr).reshape(h, w, f)
+        if pool:
+            acc = oracle.maxpool(acc, 2, 2, 2)
+        want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn.thresh, bn.ge_dir, False))
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 9 * c)
+    w8 = _dev.widen_i8(_dev.upload(wt), f, 9 * c)
+    sites = h * w // (4 if pool else 1)
+    out = _dev.upload(np.full((batch, sites, -(-f // 64)), 0xFFFFFFFFFFFFFFFF, np.uint64))
+    _lib.call("b2_tc_conv_bn_pack", _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1,
+              int(pool), th(cal), _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), np.stack(want)), (h, w, c, f, pool, batch)
