@@ -16,6 +16,9 @@
 #ifndef B2_BKS128  // K elements per stage of 128-column tiles
 #define B2_BKS128 512
 #endif
+#ifndef B2_SMALLM_TILES  // below this many 256-column tiles use 128-column ones (0: never)
+#define B2_SMALLM_TILES 74
+#endif
 #ifndef B2_BYTES_BN128  // Input8 (u8 rows) on 128-column tiles
 #define B2_BYTES_BN128 0
 #endif
@@ -228,7 +231,16 @@ int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k)
   // buys the double-buffered accumulator
   if constexpr (AM == A_BYTES) return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
 #endif
-  if (g.N > 128) return launch_bn<256, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
+  if (g.N > 128) {
+    // few tiles (small batch): 128-column tiles, 512-element stages — twice
+    // the CTAs and a quarter of the per-stage hand-offs on the serial K walk
+    if constexpr (AM == A_ROWS || AM == A_CONV) {
+      const int64_t tiles256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
+      if (B2_SMALLM_TILES && tiles256 < B2_SMALLM_TILES && (AM != A_CONV || g.spw % 4 == 0))
+        return launch_bn<128, AM, EM, 8, 512>(g, b_i8, kpad, k, st);
+    }
+    return launch_bn<256, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
+  }
   if constexpr (AM == A_BYTECONV) {
     return launch_bn<128, AM, EM, 4, 128, B2_NEPI_BYTECONV>(g, b_i8, kpad, k, st);
   } else if constexpr (AM == A_BYTES) {
