@@ -53,6 +53,11 @@ const char* b2_version(void);
 /* Number of kernel launches issued through this library since load
  * (host-side counter, for the bench's gpu_launches claim). */
 int64_t b2_launch_count(void);
+/* Programmatic dependent launch (each kernel's launch and prologue overlap
+ * the previous kernel on the stream): 1 on, 0 off.  Initially on unless the
+ * environment sets B2_PDL=0.  Returns the previous setting.  Launches
+ * already captured into a CUDA graph keep the setting they were made with. */
+int b2_set_pdl(int on);
 
 /* ---------------------------------------------------------------- packing */
 

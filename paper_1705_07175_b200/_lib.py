@@ -39,6 +39,7 @@ class Thresh(ctypes.Structure):
 SIGNATURES = {
     "b2_version": (ctypes.c_char_p, []),
     "b2_launch_count": (i64, []),
+    "b2_set_pdl": (cint, [cint]),
     "b2_pack_lines_f32": (cint, [vp, i64, i64, vp, vp]),
     "b2_unpack_lines_f32": (cint, [vp, i64, i64, vp, vp]),
     "b2_pack_byte_planes": (cint, [vp, i64, i64, vp, vp]),
@@ -116,6 +117,11 @@ def version() -> str:
 
 def launch_count() -> int:
     return int(_so.b2_launch_count())
+
+
+def set_pdl(on: bool) -> bool:
+    """Programmatic dependent launch on/off; returns the previous setting."""
+    return bool(_so.b2_set_pdl(1 if on else 0))
 
 
 def exported_symbols() -> list[str]:

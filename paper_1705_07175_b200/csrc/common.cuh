@@ -21,6 +21,50 @@ inline int launched() {
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch: every kernel is launched with
+// programmatic stream serialization, so its launch, CTA placement and
+// prologue overlap the tail of the kernel before it on the stream (the
+// per-layer chain of a forward pass at batch 1 is mostly that latency).
+// Each kernel calls griddepcontrol.wait before it touches global memory the
+// previous kernel may read or write, and releases its own dependents right
+// after.  B2_PDL=0 launches plainly (both instructions are then no-ops).
+bool pdl_enabled();
+// `cluster` > 1: thread-block clusters of that many CTAs along x
+template <typename... KArgs, typename... Args>
+inline void launch_kc(int cluster, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args... args) {
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = (unsigned)cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n++].val.clusterDim.z = 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  cudaLaunchKernelEx(&cfg, kern, args...);  // errors surface through launched()
+}
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  launch_kc(1, kern, grid, block, smem, st, args...);
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() {
+  pdl_wait();
+  pdl_trigger();
+}
+
 // Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device,
 // once per (kernel, device): the attribute is per device, and one process
 // may drive several GPUs.  `done` is the caller's per-kernel static bitmask.

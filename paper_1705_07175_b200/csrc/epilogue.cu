@@ -11,6 +11,7 @@ namespace b2 {
 // _kernels.py:224-240 maxpool, batched int32 (batch, h, w, c)
 __global__ void k_maxpool_i32(const int32_t* __restrict__ x, int64_t batch, int h, int w, int c, int ph, int pw,
                               int stride, int h_out, int w_out, int32_t* __restrict__ out) {
+  pdl_entry();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = batch * h_out * w_out * c;
   if (t >= total) return;
@@ -45,6 +46,7 @@ template <typename T>
 __global__ void k_threshold_pack(const void* __restrict__ x, int64_t batch, int64_t sites, int64_t c,
                                  const int64_t* __restrict__ thresh, const uint8_t* __restrict__ ge, int flat,
                                  int64_t line_words32, int64_t lines_per_img, uint32_t* __restrict__ out) {
+  pdl_entry();
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t words = batch * lines_per_img * line_words32;
   if (warp >= words) return;
@@ -78,6 +80,7 @@ template <typename T>
 __global__ void k_bn_affine(const void* __restrict__ x, int64_t n, const double* __restrict__ mean,
                             const double* __restrict__ scale, const double* __restrict__ beta, int64_t c,
                             double* __restrict__ out) {
+  pdl_entry();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t ch = i % c;
@@ -95,6 +98,7 @@ __global__ void k_bn_calibrate(const float* __restrict__ mean, const float* __re
                                const float* __restrict__ gamma, const float* __restrict__ beta, double eps, int64_t c,
                                int64_t bound, double* __restrict__ scale64, int64_t* __restrict__ thresh64,
                                uint8_t* __restrict__ ge_dir, int32_t* __restrict__ thresh32) {
+  pdl_entry();
   int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ch >= c) return;
   const int64_t ALWAYS = -(1LL << 62), NEVER = 1LL << 62, SB = 1LL << 40;
@@ -139,6 +143,7 @@ __global__ void k_bn_calibrate(const float* __restrict__ mean, const float* __re
 }
 
 __global__ void k_add_corr(int32_t* __restrict__ acc, const int32_t* __restrict__ corr, int64_t n, int64_t per) {
+  pdl_entry();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) acc[i] += corr[i % per];
 }
@@ -155,7 +160,7 @@ int b2_maxpool_i32(const int32_t* x, int64_t batch, int h, int w, int c, int ph,
   int h_out = (h - ph) / stride + 1, w_out = (w - pw) / stride + 1;
   int64_t n = batch * h_out * w_out * c;
   if (!n) return 0;
-  k_maxpool_i32<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(x, batch, h, w, c, ph, pw, stride, h_out, w_out, out);
+  launch_k(k_maxpool_i32, (unsigned)cdiv(n, 256), 256, 0, S(stream), x, batch, h, w, c, ph, pw, stride, h_out, w_out, out);
   return launched();
 }
 
@@ -169,13 +174,13 @@ int b2_threshold_pack(const void* x, int xkind, int64_t batch, int64_t sites, in
   unsigned grid = (unsigned)cdiv(words, 8);
   cudaStream_t st = S(stream);
   if (xkind == 0)
-    k_threshold_pack<int32_t><<<grid, 256, 0, st>>>(x, batch, sites, c, th.thresh64, th.ge_dir, flat, lw32, lines,
+    launch_k(k_threshold_pack<int32_t>, grid, 256, 0, st, x, batch, sites, c, th.thresh64, th.ge_dir, flat, lw32, lines,
                                                     (uint32_t*)out);
   else if (xkind == 1)
-    k_threshold_pack<int64_t><<<grid, 256, 0, st>>>(x, batch, sites, c, th.thresh64, th.ge_dir, flat, lw32, lines,
+    launch_k(k_threshold_pack<int64_t>, grid, 256, 0, st, x, batch, sites, c, th.thresh64, th.ge_dir, flat, lw32, lines,
                                                     (uint32_t*)out);
   else
-    k_threshold_pack<uint8_t><<<grid, 256, 0, st>>>(x, batch, sites, c, th.thresh64, th.ge_dir, flat, lw32, lines,
+    launch_k(k_threshold_pack<uint8_t>, grid, 256, 0, st, x, batch, sites, c, th.thresh64, th.ge_dir, flat, lw32, lines,
                                                     (uint32_t*)out);
   return launched();
 }
@@ -186,11 +191,11 @@ int b2_bn_affine_f64(const void* x, int xkind, int64_t n, const double* mean, co
   if (!n) return 0;
   unsigned grid = (unsigned)cdiv(n, 256);
   if (xkind == 0)
-    k_bn_affine<int32_t><<<grid, 256, 0, S(stream)>>>(x, n, mean, scale, beta, c, out);
+    launch_k(k_bn_affine<int32_t>, grid, 256, 0, S(stream), x, n, mean, scale, beta, c, out);
   else if (xkind == 1)
-    k_bn_affine<int64_t><<<grid, 256, 0, S(stream)>>>(x, n, mean, scale, beta, c, out);
+    launch_k(k_bn_affine<int64_t>, grid, 256, 0, S(stream), x, n, mean, scale, beta, c, out);
   else
-    k_bn_affine<double><<<grid, 256, 0, S(stream)>>>(x, n, mean, scale, beta, c, out);
+    launch_k(k_bn_affine<double>, grid, 256, 0, S(stream), x, n, mean, scale, beta, c, out);
   return launched();
 }
 
@@ -198,7 +203,7 @@ int b2_bn_calibrate(const float* mean, const float* var, const float* gamma, con
                     int64_t bound, double* scale64, int64_t* thresh64, uint8_t* ge_dir, int32_t* thresh32,
                     void* stream) {
   if (c < 1 || bound < 0 || bound > (1LL << 31) - 2 || !thresh64 || !ge_dir) return B2_EINVAL;
-  k_bn_calibrate<<<(unsigned)cdiv(c, 128), 128, 0, S(stream)>>>(mean, var, gamma, beta, eps, c, bound, scale64,
+  launch_k(k_bn_calibrate, (unsigned)cdiv(c, 128), 128, 0, S(stream), mean, var, gamma, beta, eps, c, bound, scale64,
                                                                 thresh64, ge_dir, thresh32);
   return launched();
 }
@@ -206,7 +211,7 @@ int b2_bn_calibrate(const float* mean, const float* var, const float* gamma, con
 int b2_add_correction_i32(int32_t* acc, const int32_t* corr, int64_t n, int64_t per_image, void* stream) {
   if (n < 0 || per_image < 1) return B2_EINVAL;
   if (!n) return 0;
-  k_add_corr<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(acc, corr, n, per_image);
+  launch_k(k_add_corr, (unsigned)cdiv(n, 256), 256, 0, S(stream), acc, corr, n, per_image);
   return launched();
 }
 

@@ -13,7 +13,7 @@ int launch_gemm(const GemmArgs& g, cudaStream_t st) {
   smem_optin(kern, Cfg::SMEM, attr);
   if (g.M == 0 || g.N == 0) return 0;
   dim3 grid((unsigned)cdiv(g.M, Cfg::BM), (unsigned)cdiv(g.N, Cfg::BN));
-  kern<<<grid, 256, Cfg::SMEM, st>>>(g);
+  launch_k(kern, grid, 256, Cfg::SMEM, st, g);
   return launched();
 }
 
@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(256) k_dense_small(const uint32_t* __restrict_
                                                     int kw32, int32_t kbits, int32_t* __restrict__ out,
                                                     uint32_t* __restrict__ out_bits, int64_t ldo32,
                                                     const int32_t* __restrict__ thresh, const uint8_t* __restrict__ ge) {
+  pdl_entry();
   __shared__ int32_t res[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ubase = (int64_t)blockIdx.x * 32;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) k_dense_small(const uint32_t* __restrict_
 // word of an unrolled row; window cells are copied as bit runs.
 __global__ void k_unroll(const uint64_t* __restrict__ lines, int64_t batch, int h, int w, int c, int kh, int kw,
                          int stride, int pad, int h_out, int w_out, int64_t row_words, uint64_t* __restrict__ out) {
+  pdl_entry();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t rows = batch * h_out * w_out;
   if (t >= rows * row_words) return;
@@ -121,6 +123,7 @@ __global__ void k_unroll(const uint64_t* __restrict__ lines, int64_t batch, int 
 // +/-1 weights over the window cells lying in the padding ring.
 __global__ void k_correction(const uint64_t* __restrict__ wwords, int64_t filters, int h, int w, int c, int kh,
                              int kw, int stride, int pad, int h_out, int w_out, int32_t* __restrict__ corr) {
+  pdl_entry();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)h_out * w_out * filters) return;
   int64_t pos = t / filters, f = t % filters;
@@ -190,7 +193,7 @@ int b2_bgemv(const uint64_t* w, int64_t units, int64_t wpl, const uint64_t* x, i
   if (units < 0 || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl) return B2_EINVAL;
   if (!units || !batch) return 0;
   if (batch <= 8) {
-    k_dense_small<false><<<(unsigned)cdiv(units, 32), 256, 0, S(stream)>>>(
+    launch_k(k_dense_small<false>, (unsigned)cdiv(units, 32), 256, 0, S(stream), 
         (const uint32_t*)x, batch, 2 * wpl, (const uint32_t*)w, units, 2 * wpl, (int)(2 * wpl), k, out, nullptr, 0,
         nullptr, nullptr);
     return launched();
@@ -205,7 +208,7 @@ int b2_dense_bn_pack(const uint64_t* x, int64_t batch, const uint64_t* w, int64_
   int64_t ldo32 = 2 * wpl64(units);
   if (batch <= 8) {
     // one block per output word, padding words included (they must be written as 0)
-    k_dense_small<true><<<(unsigned)(cdiv(units, 32) > ldo32 ? cdiv(units, 32) : ldo32), 256, 0, S(stream)>>>(
+    launch_k(k_dense_small<true>, (unsigned)(cdiv(units, 32) > ldo32 ? cdiv(units, 32) : ldo32), 256, 0, S(stream), 
         (const uint32_t*)x, batch, 2 * wpl, (const uint32_t*)w, units, 2 * wpl, (int)(2 * wpl), k, nullptr,
         (uint32_t*)out, ldo32, th.thresh, th.ge_dir);
     return launched();
@@ -235,7 +238,7 @@ int b2_unroll_packed(const uint64_t* lines, int64_t batch, int h, int w, int c, 
   int64_t row_words = wpl64((int64_t)kh * kw * c);
   int64_t n = batch * h_out * w_out * row_words;
   if (!n) return 0;
-  k_unroll<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(lines, batch, h, w, c, kh, kw, stride, pad, h_out, w_out,
+  launch_k(k_unroll, (unsigned)cdiv(n, 256), 256, 0, S(stream), lines, batch, h, w, c, kh, kw, stride, pad, h_out, w_out,
                                                            row_words, out);
   return launched();
 }
@@ -246,7 +249,7 @@ int b2_conv_correction(const uint64_t* wwords, int64_t filters, int h, int w, in
   if (h + 2 * pad < kh || w + 2 * pad < kw) return B2_EINVAL;
   int h_out = (h + 2 * pad - kh) / stride + 1, w_out = (w + 2 * pad - kw) / stride + 1;
   int64_t n = (int64_t)h_out * w_out * filters;
-  k_correction<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(wwords, filters, h, w, c, kh, kw, stride, pad, h_out,
+  launch_k(k_correction, (unsigned)cdiv(n, 256), 256, 0, S(stream), wwords, filters, h, w, c, kh, kw, stride, pad, h_out,
                                                               w_out, corr);
   return launched();
 }

@@ -86,6 +86,7 @@ __device__ __forceinline__ void conv_row(const GemmArgs& g, int64_t m, int64_t& 
 
 template <class Cfg, int CWA, int CWB, bool CONV, int MODE, int TM, int TN, int WARPS_N>
 __global__ void __launch_bounds__(256, 2) k_popc_gemm(const GemmArgs g) {
+  pdl_entry();
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, LDS = Cfg::LDS, STAGES = Cfg::STAGES;
   constexpr int A_CPR = BK / CWA;  // A chunks per row per stage
   constexpr int A_CHUNKS = BM * A_CPR / 256;

@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) k_input8_bn_pack(const uint8_t* __restric
                                                        int64_t ldw, const int32_t* __restrict__ thresh,
                                                        const uint8_t* __restrict__ ge, uint32_t* __restrict__ out,
                                                        int64_t ldo32) {
+  pdl_entry();
   extern __shared__ uint32_t sm[];
   const int pitchw = kw32 | 1;  // odd pitch: lanes hit distinct banks
   uint32_t* P = sm;                                   // [I8_IMG][8][kw32]
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(256) k_input8_bn_pack(const uint8_t* __restric
 // planes are laid out (8, batch, wpl) as produced by b2_pack_byte_planes.
 __global__ void k_bitplane_gemv(const uint64_t* __restrict__ planes, int64_t batch, const uint64_t* __restrict__ w,
                                 int64_t units, int64_t wpl, int64_t* __restrict__ out) {
+  pdl_entry();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= batch * units) return;
   int64_t img = t / units, u = t % units;
@@ -127,6 +129,7 @@ __global__ void __launch_bounds__(256) k_byte_conv_bn_pack(const uint8_t* __rest
                                                           int w_out, const int32_t* __restrict__ tout,
                                                           const uint8_t* __restrict__ gout, uint32_t* __restrict__ out,
                                                           int ldo32) {
+  pdl_entry();
   extern __shared__ uint32_t sm[];
   uint32_t* sites = sm;                 // [h*w] c-bit site codes
   uint32_t* wf = sites + h * w;         // [ngroups*32] filter words
@@ -195,7 +198,7 @@ int b2_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const uint64_t
   static std::atomic<uint64_t> attr{0};
   smem_optin(k_input8_bn_pack, 200 * 1024, attr);
   dim3 grid((unsigned)cdiv(batch, I8_IMG), (unsigned)cdiv(units, 32 * I8_TN));
-  k_input8_bn_pack<<<grid, 256, smem, S(stream)>>>(x, batch, (int)k, kw32, (const uint32_t*)w, units, kw32,
+  launch_k(k_input8_bn_pack, grid, 256, smem, S(stream), x, batch, (int)k, kw32, (const uint32_t*)w, units, kw32,
                                                    th.thresh, th.ge_dir, (uint32_t*)out, 2 * wpl64(units));
   return launched();
 }
@@ -205,7 +208,7 @@ int b2_bitplane_gemv(const uint64_t* planes, int64_t batch, const uint64_t* w, i
   if (batch < 0 || units < 0 || wpl < 1) return B2_EINVAL;
   int64_t n = batch * units;
   if (!n) return 0;
-  k_bitplane_gemv<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(planes, batch, w, units, wpl, out);
+  launch_k(k_bitplane_gemv, (unsigned)cdiv(n, 256), 256, 0, S(stream), planes, batch, w, units, wpl, out);
   return launched();
 }
 
@@ -226,7 +229,7 @@ int b2_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b
   static std::atomic<uint64_t> attr{0};
   smem_optin(k_byte_conv_bn_pack, 200 * 1024, attr);
   int64_t ldw = 2 * wpl64((int64_t)kh * kw * c);
-  k_byte_conv_bn_pack<<<(unsigned)batch, 256, smem, S(stream)>>>(x, h, w, c, th_in.thresh, th_in.ge_dir,
+  launch_k(k_byte_conv_bn_pack, (unsigned)batch, 256, smem, S(stream), x, h, w, c, th_in.thresh, th_in.ge_dir,
                                                                  (const uint32_t*)wwords, ldw, (int)filters, kh, kw,
                                                                  stride, pad, h_out, w_out, th_out.thresh,
                                                                  th_out.ge_dir, (uint32_t*)out, ldo32);

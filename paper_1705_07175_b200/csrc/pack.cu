@@ -4,11 +4,26 @@
 // 32*j + i, so ballot bit i is element i of the word — exactly the
 // reference's LSB-first order (_kernels.py:6-9).  Lines are padded to whole
 // uint64 words; lanes past the line length vote 0, so padding bits are zero.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace b2 {
 
 std::atomic<int64_t> g_launches{0};
+
+// programmatic dependent launch on (1) / off (0); B2_PDL in the environment
+// sets the initial value, b2_set_pdl() changes it
+static std::atomic<int> g_pdl{-1};
+bool pdl_enabled() {
+  int v = g_pdl.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("B2_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_pdl.store(v, std::memory_order_relaxed);
+  }
+  return v != 0;
+}
 
 // _kernels.py:43-54 pack_lines: bit = !(x < 0)  (0.0, -0.0 and NaN -> 1).
 // HBM-bound (4 B in, 1/8 B out per element).  One warp packs 32 words of one
@@ -18,6 +33,7 @@ std::atomic<int64_t> g_launches{0};
 // of a pass are independent (full unroll), keeping enough bytes in flight.
 __global__ void __launch_bounds__(256) k_pack_lines_f32(const float* __restrict__ lines, int64_t n_lines,
                                                         int64_t bits, int64_t wpl32, uint32_t* __restrict__ out) {
+  pdl_entry();
   const int64_t chunks_per_line = (wpl32 + 31) / 32;
   const int64_t chunks = n_lines * chunks_per_line;
   const int lane = lane_id();
@@ -45,6 +61,7 @@ __global__ void __launch_bounds__(256) k_pack_lines_f32(const float* __restrict_
 // _kernels.py:57-64 unpack_lines
 __global__ void k_unpack_lines_f32(const uint32_t* __restrict__ words, int64_t n_lines, int64_t bits, int64_t wpl32,
                                    float* __restrict__ out) {
+  pdl_entry();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_lines * bits) return;
   int64_t line = i / bits, b = i % bits;
@@ -65,6 +82,7 @@ __device__ __forceinline__ uint32_t plane_nibble(uint32_t v, int p) {
 // neighbour's mask into the plane's 32-bit word.
 __global__ void __launch_bounds__(256) k_pack_byte_planes(const uint8_t* __restrict__ lines, int64_t n_lines,
                                                           int64_t bits, int64_t wpl32, uint32_t* __restrict__ out) {
+  pdl_entry();
   const int64_t chunks_per_line = (wpl32 + 15) / 16;
   const int64_t chunks = n_lines * chunks_per_line;
   const int lane = lane_id();
@@ -102,6 +120,11 @@ extern "C" {
 
 const char* b2_version(void) { return "bitnn_b200 0.1 (sm_100a)"; }
 int64_t b2_launch_count(void) { return g_launches.load(); }
+int b2_set_pdl(int on) {
+  const int was = pdl_enabled() ? 1 : 0;
+  g_pdl.store(on ? 1 : 0, std::memory_order_relaxed);
+  return was;
+}
 
 int b2_pack_lines_f32(const float* lines, int64_t n_lines, int64_t bits, uint64_t* out, void* stream) {
   if (n_lines < 0 || bits < 1) return B2_EINVAL;
@@ -109,7 +132,7 @@ int b2_pack_lines_f32(const float* lines, int64_t n_lines, int64_t bits, uint64_
   int64_t chunks = n_lines * cdiv(wpl32, 32);
   if (!chunks) return 0;
   const int64_t blocks = cdiv(chunks, 8) < 148 * 32 ? cdiv(chunks, 8) : 148 * 32;  // grid-stride beyond
-  k_pack_lines_f32<<<(unsigned)blocks, 256, 0, S(stream)>>>(lines, n_lines, bits, wpl32, (uint32_t*)out);
+  launch_k(k_pack_lines_f32, (unsigned)blocks, 256, 0, S(stream), lines, n_lines, bits, wpl32, (uint32_t*)out);
   return launched();
 }
 
@@ -117,7 +140,7 @@ int b2_unpack_lines_f32(const uint64_t* words, int64_t n_lines, int64_t bits, fl
   if (n_lines < 0 || bits < 1) return B2_EINVAL;
   int64_t n = n_lines * bits;
   if (!n) return 0;
-  k_unpack_lines_f32<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>((const uint32_t*)words, n_lines, bits,
+  launch_k(k_unpack_lines_f32, (unsigned)cdiv(n, 256), 256, 0, S(stream), (const uint32_t*)words, n_lines, bits,
                                                                     2 * wpl64(bits), out);
   return launched();
 }
@@ -128,7 +151,7 @@ int b2_pack_byte_planes(const uint8_t* lines, int64_t n_lines, int64_t bits, uin
   int64_t chunks = n_lines * cdiv(wpl32, 16);
   if (!chunks) return 0;
   const int64_t blocks = cdiv(chunks, 8) < 148 * 32 ? cdiv(chunks, 8) : 148 * 32;  // grid-stride beyond
-  k_pack_byte_planes<<<(unsigned)blocks, 256, 0, S(stream)>>>(lines, n_lines, bits, wpl32, (uint32_t*)out);
+  launch_k(k_pack_byte_planes, (unsigned)blocks, 256, 0, S(stream), lines, n_lines, bits, wpl32, (uint32_t*)out);
   return launched();
 }
 

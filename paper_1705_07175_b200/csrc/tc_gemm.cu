@@ -5,6 +5,8 @@
 
 #include <mutex>
 
+#include <stdlib.h>
+
 #include "tc_i8.cuh"
 
 #ifndef B2_RESIDENT_B
@@ -15,6 +17,9 @@
 #endif
 #ifndef B2_BKS128  // K elements per stage of 128-column tiles
 #define B2_BKS128 512
+#endif
+#ifndef B2_SPLITK  // cluster split-K for few-tile launches (0: off)
+#define B2_SPLITK 1
 #endif
 #ifndef B2_SMALLM_TILES  // below this many 256-column tiles use 128-column ones (0: never)
 #define B2_SMALLM_TILES 74
@@ -35,6 +40,7 @@ namespace tc {
 // widen32 (perm_pos); without it (u8 A operand) K stays in order.
 __global__ void k_expand_i8(const uint64_t* __restrict__ w, int64_t rows, int64_t wpl, int64_t k, int64_t kpad,
                             int permute, int8_t* __restrict__ out) {
+  pdl_entry();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one thread per 4 output bytes
   int64_t per_row = kpad / 4;
   if (t >= rows * per_row) return;
@@ -80,6 +86,7 @@ __global__ void __launch_bounds__(256) k_byte_unroll(const uint8_t* __restrict__
                                                      int kw_, int stride, int pad, int ho, int wo, int kw32,
                                                      int pooled, const int32_t* __restrict__ t,
                                                      const uint8_t* __restrict__ ge, uint32_t* __restrict__ out) {
+  pdl_entry();
   const int c = C ? C : c_, kh = KH ? KH : kh_, kw = KW ? KW : kw_;
   extern __shared__ uint8_t codes[];  // [in_rows][w]
   const int bands = (ho + BAND - 1) / BAND;  // grid = images x bands, flattened (no 65535 cap)
@@ -197,23 +204,55 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4)>
+// KS: split-K over thread-block clusters of g.ksplit CTAs (one tile's K
+// splits), one work item per CTA.
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4), bool KS = false>
 int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st) {
   g.nkb = (int)((k + BKS - 1) / BKS);
   g.klast = (int)(((k - 1) % BKS) / 32 + 1);
   // one N tile whose every K stage fits the B ring space: keep it resident
-  g.resb = (g.N <= BN && (int64_t)g.nkb * BN * BKS <= (int64_t)b_stages<BN, BKS>() * BN * BKS &&
+  g.resb = (!KS && g.N <= BN && (int64_t)g.nkb * BN * BKS <= (int64_t)b_stages<BN, BKS>() * BN * BKS &&
             B2_RESIDENT_B) ? 1 : 0;
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, kpad, BN)) return rc;
-  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI>;
+  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS>;
   constexpr int smem = smem_bytes<BN, AM, BKS>();
   static std::atomic<uint64_t> attr{0};
   smem_optin(kern, smem, attr);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-  int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, num_threads<NPW, NEPI>(), smem, st>>>(map, g);
+  if constexpr (KS) {
+    launch_kc(g.ksplit, kern, (unsigned)(tiles * g.ksplit), num_threads<NPW, NEPI>(), smem, st, map, g);
+  } else {
+    g.ksplit = 1;
+    int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    launch_k(kern, grid, num_threads<NPW, NEPI>(), smem, st, map, g);
+  }
   return launched();
+}
+
+// Split-K for launches with few tiles (small batches) and deep K: the ks K
+// splits of each 128x128 tile run as one cluster and reduce over distributed
+// shared memory, so the serial K walk of a deep layer spreads over ks SMs.
+// Returns the split count (0: not applicable).
+template <int AM, int EM>
+int splitk_count(const Args& g, int64_t k) {
+  if constexpr ((EM == E_PACK || EM == E_POOLPACK) && (AM == A_ROWS || AM == A_CONV)) {
+    static const int on = [] {
+      const char* e = getenv("B2_SPLITK");
+      return e ? atoi(e) : B2_SPLITK;
+    }();
+    if (!on) return 0;
+    if (AM == A_CONV && g.spw % 4 != 0) return 0;
+    const int64_t ntiles = (g.N + 127) / 128;
+    const int64_t tiles = ((g.M + BM - 1) / BM) * ntiles;
+    const int64_t nkb = (k + 511) / 512;
+    // the cluster launch, its two barriers and the exchange cost ~3 us
+    // (measured, graph-replayed): worth it only for long K walks
+    if (nkb < 8 || ntiles * 128 > THR_COLS || 2 * tiles > num_sms()) return 0;
+    for (int ks = 8; ks >= 2; ks /= 2)
+      if (ks <= nkb && tiles * ks <= num_sms()) return ks;
+  }
+  return 0;
 }
 
 // N <= 128: 128-column tiles, double-buffered accumulator, 512-element K
@@ -226,6 +265,12 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
 template <int AM, int EM>
 int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k) {
   if (g.M == 0 || g.N == 0) return 0;
+  if (int ks = splitk_count<AM, EM>(g, k)) {
+    if constexpr ((EM == E_PACK || EM == E_POOLPACK) && (AM == A_ROWS || AM == A_CONV)) {
+      g.ksplit = ks;
+      return launch_bn<128, AM, EM, 8, 512, 4, true>(g, b_i8, kpad, k, st);
+    }
+  }
 #if B2_BYTES_BN128
   // u8 rows need no widening: re-reading A per 128-column tile is cheap and
   // buys the double-buffered accumulator
@@ -297,7 +342,7 @@ int b2_expand_i8(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, int pe
   int64_t kpad = tc::kpad_of(k);
   int64_t n = rows * kpad / 4;
   if (!n) return 0;
-  tc::k_expand_i8<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(w, rows, wpl, k, kpad, permute, out);
+  launch_k(tc::k_expand_i8, (unsigned)cdiv(n, 256), 256, 0, S(stream), w, rows, wpl, k, kpad, permute, out);
   return launched();
 }
 
@@ -413,7 +458,7 @@ int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c
     const size_t smem = (size_t)in_rows * w;
     if (smem > 48 * 1024 || batch * bands > INT32_MAX) return B2_EINVAL;
     auto kern = (kh == 3 && kw == 3 && c == 3) ? tc::k_byte_unroll<3, 3, 3> : tc::k_byte_unroll<0, 0, 0>;
-    kern<<<(unsigned)(batch * bands), 256, smem, S(stream)>>>(
+    launch_k(kern, (unsigned)(batch * bands), 256, smem, S(stream), 
         x, h, w, c, kh, kw, stride, pad, g.Ho, g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
         reinterpret_cast<uint32_t*>(scratch));
   }

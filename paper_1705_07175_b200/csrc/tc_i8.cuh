@@ -66,6 +66,7 @@ struct Args {
   int klast;  // K=32 MMAs carrying data in the last stage (1..BKS/32)
   int resb;   // the whole B tile (all K stages) stays resident in shared memory:
               // loaded once per CTA (one N tile, nkb stages fit the ring space)
+  int ksplit; // split-K kernels: K splits per tile = cluster size (2/4/8)
   // ---- epilogue
   int32_t* out_i32;
   int64_t ldo;
@@ -150,6 +151,28 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint32_t a_tmem, uint
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// ---- thread-block cluster (split-K reduction over distributed shared memory)
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_map(uint32_t saddr, uint32_t rank) {  // my smem address -> rank's
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+// Work item t of a kernel with ksp K splits per tile: tile t / ksp, K
+// stages [kb0, kb1) of split t % ksp (ksp = 1: the whole K walk).
+__device__ __forceinline__ void item_krange(const Args& g, int ksp, int64_t t, int& kb0, int& kb1) {
+  const int s = (int)(t % ksp);
+  kb0 = s * g.nkb / ksp;
+  kb1 = (s + 1) * g.nkb / ksp;
 }
 
 #define B2_R32(v)                                                                                                   \
@@ -256,18 +279,19 @@ __device__ __forceinline__ void widen32m(uint32_t x, uint32_t valid, uint32_t* o
 //   A_BYTES:                      64 raw bytes (4 x uint4)
 template <int AM, bool POOLED, int WS, int TW>  // WS = K words per stage, TW = words per producer thread
 struct ACursor {
-  int64_t t;       // tile of the next fetch
-  int kb;          // K block of the next fetch
+  int64_t t;       // work item of the next fetch (tile t / ksp)
+  int kb, kend;    // K block of the next fetch, end of the item's K range
   bool mok;        // row inside M
   const uint32_t* base;
   int iy0, ix0;    // conv: window origin of this row
   int cell, within, dy, dx;  // conv: window cell and word of this half's next K words
   int64_t img;
 
-  __device__ __forceinline__ void tile_setup(const Args& g, int64_t mtiles, int64_t tiles, int r, int half) {
-    kb = 0;
-    const int64_t m = (t % mtiles) * BM + r;
-    mok = t < tiles && m < g.M;
+  __device__ __forceinline__ void tile_setup(const Args& g, int64_t mtiles, int64_t tiles, int r, int half,
+                                             int ksp) {
+    item_krange(g, ksp, t, kb, kend);
+    const int64_t m = (t / ksp % mtiles) * BM + r;
+    mok = t < tiles * ksp && m < g.M;
     if constexpr (AM == A_CONV) {
       img = 0;
       int oy = 0, ox = 0;
@@ -276,7 +300,7 @@ struct ACursor {
       ix0 = ox * g.stride - g.pad;
       base = g.a + img * (int64_t)g.H * g.W * g.sstride;
       cell = dy = dx = 0;
-      within = TW * half;  // this producer warp's first word of each stage
+      within = TW * half + kb * WS;  // this producer warp's first word of the item's first stage
       while (within >= g.spw) within -= g.spw, step_cell(g);
     } else {
       base = g.a + (mok ? m : 0) * g.lda;
@@ -286,15 +310,16 @@ struct ACursor {
     ++cell;
     if (++dx == g.kw) dx = 0, ++dy;
   }
-  __device__ __forceinline__ void start(const Args& g, int64_t t0, int64_t mtiles, int64_t tiles, int r, int half) {
+  __device__ __forceinline__ void start(const Args& g, int64_t t0, int64_t mtiles, int64_t tiles, int r, int half,
+                                        int ksp) {
     t = t0;
-    tile_setup(g, mtiles, tiles, r, half);
+    tile_setup(g, mtiles, tiles, r, half, ksp);
   }
   __device__ __forceinline__ void advance(const Args& g, int64_t step, int64_t mtiles, int64_t tiles, int r,
-                                          int half) {
-    if (++kb == g.nkb) {
+                                          int half, int ksp) {
+    if (++kb == kend) {
       t += step;
-      tile_setup(g, mtiles, tiles, r, half);
+      tile_setup(g, mtiles, tiles, r, half, ksp);
     } else if constexpr (AM == A_CONV) {
       within += WS;
       while (within >= g.spw) within -= g.spw, step_cell(g);
@@ -507,6 +532,30 @@ __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncol
   }
 }
 
+// Packed sign word of 32 accumulators: bit j = (v[j] * mul_j + add_j >= 0)
+// with trow = the columns' (mul, add) pairs (sign bits MSB first, reversed).
+__device__ __forceinline__ uint32_t thr_word(const uint32_t (&v)[32], const int4* trow) {
+  uint32_t sg = 0;
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const int4 p = trow[j / 2];
+    const int d0 = (int)v[j] * p.x + p.y;
+    const int d1 = (int)v[j + 1] * p.z + p.w;
+    sg = __funnelshift_l((uint32_t)d0, sg, 1);
+    sg = __funnelshift_l((uint32_t)d1, sg, 1);
+  }
+  return ~__brev(sg);
+}
+// 2x2 max-pool of thresholded rows held by 4 consecutive lanes: max then
+// threshold == OR (ge columns, mask gm) / AND (le) of the four words
+__device__ __forceinline__ uint32_t pool_word(uint32_t w, uint32_t gm) {
+  uint32_t o = w | __shfl_xor_sync(0xffffffffu, w, 1);
+  o |= __shfl_xor_sync(0xffffffffu, o, 2);
+  uint32_t a = w & __shfl_xor_sync(0xffffffffu, w, 1);
+  a &= __shfl_xor_sync(0xffffffffu, a, 2);
+  return (o & gm) | (a & ~gm);
+}
+
 // ------------------------------------------------------------------ kernel
 template <int NPW, int NEPI>
 constexpr int num_threads() {
@@ -520,7 +569,7 @@ constexpr int num_threads() {
 // quarter, half the columns each: TMEM reads are latency-bound per warp,
 // ~42 B/clk each, so a single-buffered 256-column accumulator drains twice
 // as fast).
-template <int BN, int AM, int EM, int NPW, int BKS, int NEPI>
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS>
 __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
                                                                   const Args g) {
   constexpr int WS = BKS / 32;        // K words per stage
@@ -562,10 +611,15 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   const int64_t mtiles = (g.M + BM - 1) / BM;
   const int ntiles = (g.N + BN - 1) / BN;
   const int64_t tiles = mtiles * ntiles;  // tile t -> (m tile t % mtiles, n tile t / mtiles)
+  // split-K (KS): the ksp K splits of a tile are the ranks of one cluster;
+  // work item t -> tile t / ksp, split t % ksp; one item per CTA
+  const int ksp = KS ? g.ksplit : 1;
+  const int64_t items = tiles * ksp;
+  const bool resb = !KS && g.resb;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&full[s], NPW + (g.resb ? 0 : 1));  // every A-producer warp (+ the TMA expect_tx arrival)
+      mbar_init(&full[s], NPW + (resb ? 0 : 1));  // every A-producer warp (+ the TMA expect_tx arrival)
       mbar_init(&empty[s], 1);
     }
     mbar_init(bres, 1);
@@ -584,28 +638,35 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // barriers, TMEM and the tensor map are set up while the previous kernel
+  // drains; every global access (weights included: a widen may have just
+  // written them) comes after the wait
+  pdl_entry();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (B)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      if constexpr (AM == A_CONV || AM == A_ROWS) {
+      if constexpr ((AM == A_CONV || AM == A_ROWS) && !KS) {
         prefetch_tile_inputs<AM>(g, blockIdx.x, mtiles, tiles);
         prefetch_tile_inputs<AM>(g, blockIdx.x + gridDim.x, mtiles, tiles);
       }
-      if (g.resb) {  // one N tile: load every K stage of B once, then only prefetch A inputs
+      if (resb) {  // one N tile: load every K stage of B once, then only prefetch A inputs
         mbar_expect_tx(bres, (uint32_t)g.nkb * B_STAGE_BYTES);
         for (int kb = 0; kb < g.nkb; ++kb)
 #pragma unroll
           for (int at = 0; at < BKS / BK; ++at)
             tma_load_2d(sb + kb * B_STAGE_BYTES + at * BN * BK, &bmap, bres, kb * BKS + at * BK, 0);
       }
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int n0 = (int)(t / mtiles) * BN;
-        if constexpr (AM == A_CONV || AM == A_ROWS) prefetch_tile_inputs<AM>(g, t + 2 * (int64_t)gridDim.x, mtiles, tiles);
-        if (g.resb) continue;
-        for (int kb = 0; kb < g.nkb; ++kb) {
+      for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+        const int n0 = (int)(t / ksp / mtiles) * BN;
+        if constexpr ((AM == A_CONV || AM == A_ROWS) && !KS)
+          prefetch_tile_inputs<AM>(g, t + 2 * (int64_t)gridDim.x, mtiles, tiles);
+        if (resb) continue;
+        int kb0, kb1;
+        item_krange(g, ksp, t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], B_STAGE_BYTES);
 #pragma unroll
@@ -622,21 +683,24 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      if (g.resb) mbar_wait(bres, 0);
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      if (resb) mbar_wait(bres, 0);
+      for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
-        for (int kb = 0; kb < g.nkb; ++kb) {
+        int kb0, kb1;
+        item_krange(g, ksp, t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
-          const uint32_t bs = smem_u32(sb + (g.resb ? kb : s) * B_STAGE_BYTES);
+          const uint32_t bs = smem_u32(sb + (resb ? kb : s) * B_STAGE_BYTES);
           const int kmma = kb + 1 == g.nkb ? g.klast : BKS / 32;
 #pragma unroll
           for (int k = 0; k < BKS / 32; ++k)
             if (k < kmma)
-              tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, (kb | k) ? 1u : 0u);
+              tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC,
+                        (kb > kb0 || k) ? 1u : 0u);
           tc_commit(&empty[s]);
           if (++s == SA) s = 0, ph ^= 1;
         }
@@ -656,9 +720,19 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     const int r = q * 32 + lane;  // tile row = TMEM lane
     const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / HALVES);
     ACursor<AM, POOLED, WS, WPH> cur;
-    cur.start(g, blockIdx.x, mtiles, tiles, r, half);
-    const int64_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t jobs = my_tiles * g.nkb;
+    cur.start(g, blockIdx.x, mtiles, tiles, r, half, ksp);
+    int64_t jobs;
+    if constexpr (KS) {
+      jobs = 0;
+      for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+        int kb0, kb1;
+        item_krange(g, ksp, t, kb0, kb1);
+        jobs += kb1 - kb0;
+      }
+    } else {
+      const int64_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      jobs = my_tiles * g.nkb;
+    }
     int s = 0, pending = -1;
     uint32_t ph = 0;
     // every stage feeds exactly one K=32 MMA (K <= 32, one stage): the first
@@ -694,7 +768,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         cur.fetch_bytes(g, half, qx[u]);
-        cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+        cur.advance(g, gridDim.x, mtiles, tiles, r, half, ksp);
       }
       for (int64_t j0 = 0; j0 < jobs; j0 += 2) {
 #pragma unroll
@@ -709,7 +783,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
               v[4 * i + 3] = qx[u][i].w;
             }
             cur.fetch_bytes(g, half, qx[u]);
-            cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+            cur.advance(g, gridDim.x, mtiles, tiles, r, half, ksp);
             publish(s, v);
             if (++s == SA) s = 0, ph ^= 1;
           }
@@ -724,7 +798,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #pragma unroll
       for (int u = 0; u < PF8; ++u) {
         cur.fetch_bits8(g, half, qx[u], qok[u]);
-        cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+        cur.advance(g, gridDim.x, mtiles, tiles, r, half, ksp);
       }
       const int ijobs = (int)jobs;
       for (int j0 = 0; j0 < ijobs; j0 += PF8) {
@@ -742,7 +816,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             }
 #endif
             cur.fetch_bits8(g, half, qx[u], qok[u]);
-            cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+            cur.advance(g, gridDim.x, mtiles, tiles, r, half, ksp);
             publish(s, v);
             if (++s == SA) s = 0, ph ^= 1;
           }
@@ -760,7 +834,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         cur.template fetch_bits<WPH>(g, half, qx[u], vm);
         if constexpr (MASKED) qv[u] = vm;
         qok[u] = vm.x != 0 || vm.y != 0 || vm.z != 0 || vm.w != 0;
-        cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+        cur.advance(g, gridDim.x, mtiles, tiles, r, half, ksp);
       }
       const int ijobs = (int)jobs;
       for (int j0 = 0; j0 < ijobs; j0 += PF) {
@@ -793,7 +867,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             cur.template fetch_bits<WPH>(g, half, qx[u], vm);
             if constexpr (MASKED) qv[u] = vm;
             qok[u] = vm.x != 0 || vm.y != 0 || vm.z != 0 || vm.w != 0;
-            cur.advance(g, gridDim.x, mtiles, tiles, r, half);
+            cur.advance(g, gridDim.x, mtiles, tiles, r, half, ksp);
             publish(s, v);
             if (++s == SA) s = 0, ph ^= 1;
           }
@@ -827,6 +901,62 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         epi_bar<NEPI>();
       }
     }
+    if constexpr (KS) {
+      // ---- split-K: reduce-scatter the ksp partial tiles over the cluster.
+      // Rank `rank` owns tile rows [rank * rpo, +rpo); every rank writes its
+      // partial of those rows into the owner's (now idle) B ring, slot
+      // [source rank][row][RS], then each owner sums its rows and packs them.
+      static_assert(EM == E_PACK || EM == E_POOLPACK, "split-K kernels pack their output");
+      constexpr int RS = BN + 4;  // padded slot row (ints): conflict-free 16-byte reads across rows
+      static_assert(BM * RS * 4 <= b_stages<BN, BKS>() * B_STAGE_BYTES, "reduction slots fit the B ring");
+      const int64_t t = blockIdx.x;  // one item per CTA
+      const int64_t tt = t / ksp;
+      const int rank = (int)(t % ksp);
+      const int rpo = BM / ksp;
+      const int n0 = (int)(tt / mtiles) * BN;
+      const int64_t mrow0 = (tt % mtiles) * BM + rank * rpo;  // first output row this rank owns
+      int32_t* slots = reinterpret_cast<int32_t*>(sb);
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
+      cluster_sync_all();  // every rank's MMAs are done: all B rings are free
+      {
+        const int owner = r / rpo, lr = r % rpo;
+        const uint32_t dst = cluster_map(smem_u32(slots + (rank * rpo + lr) * RS + ec0), (uint32_t)owner);
+#pragma unroll
+        for (int c = 0; c < ECH; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tmem + lane_addr + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            st_cluster_v4(dst + (c * 32 + 4 * i) * 4, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+      cluster_sync_all();  // all partials of my rows have landed
+      const int units = rpo * (BN / 32);  // (row, 32-column chunk), rows fastest: a pool window = 4 lanes
+      for (int u0 = 0; u0 < units; u0 += 32 * NEPI) {
+        const int u = u0 + et;
+        const bool act = u < units;
+        const int row = act ? u % rpo : 0, chunk = act ? u / rpo : 0;
+        uint32_t v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0;
+        for (int src = 0; src < ksp; ++src) {
+          const int4* p = reinterpret_cast<const int4*>(slots + (src * rpo + row) * RS + chunk * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int4 x = p[i];
+            v[4 * i] += x.x, v[4 * i + 1] += x.y, v[4 * i + 2] += x.z, v[4 * i + 3] += x.w;
+          }
+        }
+        uint32_t w = thr_word(v, sthr + ((n0 + chunk * 32) >> 1));
+        if constexpr (EM == E_POOLPACK) w = pool_word(w, sgm[(n0 >> 5) + chunk]);
+        const int64_t m = mrow0 + row;
+        const int wcol = n0 / 32 + chunk;
+        if (act && m < g.M && (!POOLED || (row & 3) == 0) && wcol < g.ldo32)
+          g.out_bits[(POOLED ? (m >> 2) : m) * g.ldo32 + wcol] = w;
+      }
+    } else
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int64_t m = (t % mtiles) * BM + r;
       const int n0 = (int)(t / mtiles) * BN;
@@ -885,27 +1015,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             }
           }
         } else {
-          // sign bits of acc * mul + add, MSB first, then reversed
-          uint32_t sg = 0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const int4 p = trow[c * 16 + j / 2];
-            const int d0 = (int)v[j] * p.x + p.y;
-            const int d1 = (int)v[j + 1] * p.z + p.w;
-            sg = __funnelshift_l((uint32_t)d0, sg, 1);
-            sg = __funnelshift_l((uint32_t)d1, sg, 1);
-          }
-          uint32_t w = ~__brev(sg);
-          if constexpr (EM == E_POOLPACK) {
-            // max over the 2x2 window then threshold == OR (ge) / AND (le)
-            // of the four thresholded rows (monotone threshold)
-            const uint32_t gm = sgm[((tcol + ec0) >> 5) + c];
-            uint32_t o = w | __shfl_xor_sync(0xffffffffu, w, 1);
-            o |= __shfl_xor_sync(0xffffffffu, o, 2);
-            uint32_t a = w & __shfl_xor_sync(0xffffffffu, w, 1);
-            a &= __shfl_xor_sync(0xffffffffu, a, 2);
-            w = (o & gm) | (a & ~gm);
-          }
+          uint32_t w = thr_word(v, trow + c * 16);
+          if constexpr (EM == E_POOLPACK) w = pool_word(w, sgm[((tcol + ec0) >> 5) + c]);
           words[c] = w;
         }
         if (c + 1 < ECH) tmem_wait_ld();
@@ -947,6 +1058,12 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     }
   }
 
+  if constexpr (KS) {
+    if (warp < EPI0) {  // the epilogue's two cluster barriers count every thread of every rank
+      cluster_sync_all();
+      cluster_sync_all();
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {

@@ -72,10 +72,15 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
     assert np.array_equal(_dev.download(out, np.int32), want)
 
 
+# the last five take the cluster split-K path (>= 8 K stages of 512, few
+# tiles): ragged N, a 2048-column output, pooled and unpooled
 @pytest.mark.parametrize("h,w,c,f,pool,batch", [(8, 8, 128, 128, True, 3), (6, 10, 64, 96, False, 2),
                                                 (16, 16, 256, 256, True, 2), (8, 8, 512, 64, False, 2),
                                                 (4, 4, 512, 512, True, 5), (32, 32, 128, 128, True, 2),
-                                                (6, 6, 64, 200, True, 3)])
+                                                (6, 6, 64, 200, True, 3),
+                                                (4, 4, 512, 512, True, 1), (8, 8, 512, 200, False, 3),
+                                                (6, 6, 512, 130, True, 2), (8, 8, 1024, 64, False, 1),
+                                                (2, 2, 512, 2048, True, 1)])
 def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch):
     rng = np.random.default_rng(5 + h + c + f)
     xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
@@ -101,8 +106,11 @@ def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch):
     assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
 
 
+# split-K cases: (1, 300, 4096), (37, 1024, 8192) and the last four (a
+# partial last K stage, M over one tile, 2048 columns)
 @pytest.mark.parametrize("batch,units,k", [(1, 300, 4096), (5, 64, 1000), (37, 1024, 8192), (200, 4096, 4096),
-                                           (129, 10, 1024), (300, 130, 300), (64, 1000, 784)])
+                                           (129, 10, 1024), (300, 130, 300), (64, 1000, 784),
+                                           (17, 64, 3600), (130, 200, 4096), (5, 2048, 16384), (3, 100, 5000)])
 def test_tc_dense_bn_pack_vs_oracle(oracle, batch, units, k):
     rng = np.random.default_rng(batch + units + k)
     x = oracle.pack_lines(rand_pm1(rng, batch, k))

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--stage", type=int, default=0, help="stage index, -1 = all")
     ap.add_argument("--batch", type=int, default=8192)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--graph", action="store_true", help="time the reps as one captured CUDA graph (no host "
+                                                         "launch overhead; what a graph-replayed forward sees)")
     ap.add_argument("--map", default=None, help="write {stage: [first, last) library launch index} JSON here "
                                                  "(one untimed launch per stage, for tools/ncu_summary.py traffic)")
     a = ap.parse_args()
@@ -52,10 +54,21 @@ def main():
         st = net.stages[i]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st.launch(net, a.batch, _dev.stream())
-        e0.record()
-        for _ in range(a.reps):
-            st.launch(net, a.batch, _dev.stream())
-        e1.record()
+        if a.graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+                for _ in range(a.reps):
+                    st.launch(net, a.batch, _dev.stream())
+            g.replay()
+            torch.cuda.synchronize()
+            e0.record()
+            g.replay()
+            e1.record()
+        else:
+            e0.record()
+            for _ in range(a.reps):
+                st.launch(net, a.batch, _dev.stream())
+            e1.record()
         torch.cuda.synchronize()
         print(f"stage {i} {st.name}: {e0.elapsed_time(e1) / a.reps:.4f} ms  launches/stage {st.launches()}")
 
