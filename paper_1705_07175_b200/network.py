@@ -58,6 +58,12 @@ class _Stage:
     name = "stage"
     out_dtype = np.uint64
 
+    is_last = False  # writes the scores (the batch-1 graph may point it at pinned host memory)
+    # as the first stage, reads the image straight from pinned host memory in
+    # the batch-1 graph: only kernels that read their input once, in parallel
+    # (each dependent host read is a PCIe round trip)
+    zero_copy_in = False
+
     def __init__(self, src):
         self.src = src
         self.out = None
@@ -69,7 +75,12 @@ class _Stage:
         self.out = _dev.empty((cap, *self.per_image()), self.out_dtype)
 
     def src_ptr(self, net):
-        return _dev.P(net._in if self.src is None else self.src.out)
+        if self.src is None:
+            return net._io_ptrs[0] if net._io_ptrs else _dev.P(net._in)
+        return _dev.P(self.src.out)
+
+    def out_ptr(self, net):
+        return net._io_ptrs[1] if (net._io_ptrs and self.is_last) else _dev.P(self.out)
 
     def launches(self) -> int:
         return 1
@@ -126,6 +137,7 @@ class _Input8Raw(_Stage):
 
 class _ByteConvFused(_Stage):
     name = "bytebn+conv+bn"
+    zero_copy_in = True  # k_byte_unroll / k_byte_conv_bn_pack stage the image bands once
 
     def __init__(self, src, in_shape, bn0, rec, bn1):
         super().__init__(src)
@@ -383,7 +395,7 @@ class _DenseFinal(_Stage):
             return
         _lib.call("b2_tc_dense_affine_f64", self.src_ptr(net), batch, _dev.P(self.dense.w8), r.units,
                   _wpl(r.input_len), r.input_len, _dev.P(self.bn["mean64"]), _dev.P(self.bn["scale64"]),
-                  _dev.P(self.bn["beta64"]), _dev.P(self.out), st)
+                  _dev.P(self.bn["beta64"]), self.out_ptr(net), st)
 
 
 class _FinalBN(_Stage):
@@ -399,7 +411,7 @@ class _FinalBN(_Stage):
 
     def launch(self, net, batch, st):
         _lib.call("b2_bn_affine_f64", self.src_ptr(net), self.xkind, batch * self.classes, _dev.P(self.bn["mean64"]),
-                  _dev.P(self.bn["scale64"]), _dev.P(self.bn["beta64"]), self.classes, _dev.P(self.out), st)
+                  _dev.P(self.bn["scale64"]), _dev.P(self.bn["beta64"]), self.classes, self.out_ptr(net), st)
 
 
 # --------------------------------------------------------------------------- network
@@ -432,6 +444,16 @@ class Network:
         _dev.require_cuda()
         self.device = _dev.device()
         self.stages = self._plan(ops)
+        # the batch-1 graph reads the image from, and writes the scores to,
+        # pinned host memory directly (mapped, UVA) when the last stage is a
+        # float64 score stage: no H2D / D2H nodes on the latency path
+        self._io_ptrs = None
+        last = self.stages[-1]
+        self._zero_copy_out = isinstance(last, (_FinalBN, _DenseFinal))
+        if self._zero_copy_out:
+            last.is_last = True
+            if isinstance(last, _DenseFinal):
+                last.final.is_last = True
         self.cap = 0
         self._graphs = {}
         self._copy_stream = None
@@ -825,16 +847,26 @@ def forward(net: Network, image: np.ndarray) -> np.ndarray:
     x = _check_image(net, image)
     net._in_host_np[0] = x.reshape(-1)
     if net.use_graphs:
-        # one graph holds H2D + the forward pass + D2H: a single launch per image
+        # one graph per image: the forward pass reading the pinned image and
+        # writing the pinned scores (zero-copy), a single launch
         g = net._graphs.get("io1")
         if g is None:
             net.run(1)  # eager warm-up + the batch-1 compute graph
             torch.cuda.current_stream().synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                net._in[:1].copy_(net._in_host[:1], non_blocking=True)
-                net._launch_all(1)
-                net._out_host[:1].copy_(net.scores_device[:1], non_blocking=True)
+            # zero-copy: the first kernel reads the pinned image, the last
+            # writes the pinned scores (a memcpy node each costs ~4-6 us)
+            zc_in = net.stages[0].zero_copy_in
+            net._io_ptrs = (_dev.P(net._in_host) if zc_in else _dev.P(net._in), _dev.P(net._out_host))
+            try:
+                with torch.cuda.graph(g):
+                    if not zc_in:
+                        net._in[:1].copy_(net._in_host[:1], non_blocking=True)
+                    net._launch_all(1)
+                    if not net._zero_copy_out:
+                        net._out_host[:1].copy_(net.scores_device[:1], non_blocking=True)
+            finally:
+                net._io_ptrs = None
             net._graphs["io1"] = g
         g.replay()
     else:
