@@ -25,6 +25,7 @@ keeps the reference's batch-1 contract and returns a reused host buffer;
 
 from __future__ import annotations
 
+import ctypes
 import enum
 
 import numpy as np
@@ -80,7 +81,9 @@ class _Stage:
         return _dev.P(self.src.out)
 
     def out_ptr(self, net):
-        return net._io_ptrs[1] if (net._io_ptrs and self.is_last) else _dev.P(self.out)
+        if net._io_ptrs and self.is_last and net._io_ptrs[1] is not None:
+            return net._io_ptrs[1]
+        return _dev.P(self.out)
 
     def launches(self) -> int:
         return 1
@@ -448,6 +451,7 @@ class Network:
         # pinned host memory directly (mapped, UVA) when the last stage is a
         # float64 score stage: no H2D / D2H nodes on the latency path
         self._io_ptrs = None
+        self._pipe_split = None  # H2D share of the per-image host->scores time (measured on first use)
         last = self.stages[-1]
         self._zero_copy_out = isinstance(last, (_FinalBN, _DenseFinal))
         if self._zero_copy_out:
@@ -744,6 +748,92 @@ class Network:
         # the array's base keeps the pinned tensor (and its allocation) alive
         return torch.empty((int(n), self.input_len), dtype=torch.uint8, pin_memory=True).numpy()
 
+    def pinned_scores(self, n: int) -> np.ndarray:
+        """A page-locked (n, classes) float64 host array: passed as
+        forward_batch's `out`, the scores are copied straight into it."""
+        return torch.empty((int(n), self.classes), dtype=torch.float64, pin_memory=True).numpy()
+
+    def _chunk_plan(self, n: int, pinned: bool) -> list:
+        """Chunks of the pipelined host path.
+
+        Pinned input (one graph per call): two chunks.  The first chunk's H2D
+        cannot overlap anything, and the second chunk's H2D must hide under
+        the first chunk's forward pass, so the first chunk is the smallest
+        multiple of 512 with c0 >= n * h / (h + t) (h, t = H2D and compute
+        time per image, measured once per network; n/8 until then).  More,
+        smaller chunks lose more to per-pass inefficiency than they gain.
+        Staged input: equal chunks that fit half the pinned workspace."""
+        if pinned:
+            f = self._pipe_split if self._pipe_split is not None else 0.125
+            c0 = max(512, -(-int(n * f) // 512) * 512)
+            return [(0, c0), (c0, n - c0)] if n - c0 >= 512 else [(0, n)]
+        ck = self.cap if self.cap < 2048 else max(1024, self.cap // 4)
+        return [(b0, min(ck, n - b0)) for b0 in range(0, n, ck)]
+
+    def _measure_pipe_split(self, n: int, src: torch.Tensor):
+        """h / (h + t) from one timed H2D of the call's input and one timed
+        forward pass over it (CUDA events, after a warm-up pass)."""
+        cur = torch.cuda.current_stream()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        self._launch_all(n)
+        e[0].record(cur)
+        self._in[:n].copy_(src[:n], non_blocking=True)
+        e[1].record(cur)
+        self._launch_all(n)
+        e[2].record(cur)
+        cur.synchronize()
+        h, t = e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])
+        self._pipe_split = min(0.5, max(0.0, h / max(h + t, 1e-9)))
+
+    _PIPE_GRAPHS = 2  # pointer-keyed whole-call graphs kept per network
+
+    def _pipe_graph(self, n: int, src: torch.Tensor, dst: torch.Tensor | None):
+        """One CUDA graph for a whole pipelined call on pinned input: the
+        copy stream forks and copies every chunk straight into its rows of
+        the workspace; the compute stream waits per chunk, runs the stages on
+        row-offset input pointers and copies the chunk's scores into the
+        pinned output (`dst`, else the pinned workspace).  No host work
+        between chunks.  None when the plan has a single chunk."""
+        key = ("pipe", n, src.data_ptr(), 0 if dst is None else dst.data_ptr())
+        g = self._graphs.get(key)
+        if g is not None:
+            return g
+        if self._pipe_split is None:
+            self._measure_pipe_split(n, src)
+        chunks = self._chunk_plan(n, True)
+        if len(chunks) < 2:
+            return None
+        for _, b in chunks:  # eager warm-up of every chunk size (lazy module / attribute work)
+            self._launch_all(b)
+        torch.cuda.current_stream().synchronize()
+        old = [k for k in self._graphs if isinstance(k, tuple) and k[0] == "pipe"]
+        for k in old[:max(0, len(old) - self._PIPE_GRAPHS + 1)]:
+            del self._graphs[k]
+        L = self.input_len
+        sink = dst if dst is not None else self._out_host
+        ready = [torch.cuda.Event() for _ in chunks]
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                cap = torch.cuda.current_stream()
+                self._copy_stream.wait_stream(cap)
+                with torch.cuda.stream(self._copy_stream):
+                    for i, (b0, b) in enumerate(chunks):
+                        self._in[b0:b0 + b].copy_(src[b0:b0 + b], non_blocking=True)
+                        ready[i].record(self._copy_stream)
+                for i, (b0, b) in enumerate(chunks):
+                    cap.wait_event(ready[i])
+                    self._io_ptrs = (ctypes.c_void_p(self._in.data_ptr() + b0 * L), None)
+                    self._launch_all(b)
+                    # a D2H node per chunk: at large batch, score kernels
+                    # writing host memory directly are slower (measured)
+                    sink[b0:b0 + b].copy_(self.scores_device[:b], non_blocking=True)
+                cap.wait_stream(self._copy_stream)
+        finally:
+            self._io_ptrs = None
+        self._graphs[key] = g
+        return g
+
     def _forward_host_block(self, images: np.ndarray, out: np.ndarray):
         n = images.shape[0]
         if n == 0:
@@ -751,11 +841,21 @@ class Network:
         compute = torch.cuda.current_stream()
         src = torch.from_numpy(images) if images.flags.c_contiguous else None
         pinned = src is not None and src.is_pinned()  # caller's page-locked memory: no host staging copy
-        ck = self.cap if self.cap < 2048 else max(1024, self.cap // 4)
-        chunks = [(b0, min(ck, n - b0)) for b0 in range(0, n, ck)]
+        dst = torch.from_numpy(out) if out.flags.c_contiguous else None
+        direct_out = dst is not None and dst.is_pinned()  # D2H straight into the caller's buffer
+        if pinned and self.use_graphs and n >= 1024:
+            g = self._pipe_graph(n, src, dst if direct_out else None)
+            if g is not None:
+                g.replay()
+                compute.synchronize()
+                if not direct_out:
+                    _parallel_copy(out[:n], self._out_host_np[:n])
+                return
+        chunks = self._chunk_plan(n, pinned)
         half = self.cap // 2 if len(chunks) > 1 else 0  # pinned rows of slot 1
         h2d_done = [torch.cuda.Event() for _ in chunks]   # staging buffer filled
         consumed = [torch.cuda.Event() for _ in chunks]   # staging buffer copied into the workspace
+        d2h_done = [torch.cuda.Event() for _ in chunks]   # chunk scores in pinned memory
 
         def stage(i):
             b0, b = chunks[i]
@@ -774,17 +874,26 @@ class Network:
                 self._staged[sl][:b].copy_(host, non_blocking=True)
                 h2d_done[i].record(self._copy_stream)
 
+        def collect(i):  # host copy of chunk i's scores (not for a pinned `out`)
+            b0, b = chunks[i]
+            d2h_done[i].synchronize()
+            out[b0:b0 + b] = self._out_host_np[b0:b0 + b]
+
         stage(0)
         for i, (b0, b) in enumerate(chunks):
             compute.wait_event(h2d_done[i])
             self._in[:b].copy_(self._staged[i % 2][:b], non_blocking=True)
             consumed[i].record(compute)
             self.run(b)
-            self._out_host[b0:b0 + b].copy_(self.scores_device[:b], non_blocking=True)
+            (dst if direct_out else self._out_host)[b0:b0 + b].copy_(self.scores_device[:b], non_blocking=True)
+            d2h_done[i].record(compute)
             if i + 1 < len(chunks):
                 stage(i + 1)  # host work overlaps the forward pass just enqueued
+            if not direct_out and i >= 1:
+                collect(i - 1)  # overlaps the forward pass of chunk i
         compute.synchronize()
-        out[:n] = self._out_host_np[:n]
+        if not direct_out:
+            collect(len(chunks) - 1)
 
 
 _COPY_POOL = None

@@ -222,6 +222,28 @@ def test_forward_batch_from_pinned_images(networks_golden):
     assert np.array_equal(forward_batch(net, pin), want[idx])
 
 
+@pytest.mark.parametrize("n,cap", [(5000, 8192), (4096, 4096), (9000, 4096)])
+def test_forward_batch_pinned_geometric_chunks(networks_golden, n, cap):
+    """Pinned input runs as one pipeline graph of two chunks (several blocks
+    when n > cap); a pinned `out` takes the scores by direct D2H, a plain
+    `out` through the pinned workspace."""
+    imgs = networks_golden["bcnn_images"]
+    want = networks_golden["bcnn_scores"]
+    idx = (np.arange(n) * 7) % imgs.shape[0]
+    net = Network(zoo.bcnn_spec(), max_batch=cap)
+    plan = net._chunk_plan(min(n, cap), True)
+    assert sum(b for _, b in plan) == min(n, cap) and len(plan) > 1
+    pin = net.pinned_images(n)
+    pin[...] = imgs[idx].reshape(n, -1)
+    out = net.pinned_scores(n)
+    out[...] = np.nan
+    assert forward_batch(net, pin, out) is out
+    assert np.array_equal(out, want[idx])
+    plain = np.full((n, net.classes), np.nan)
+    forward_batch(net, pin, plain)
+    assert np.array_equal(plain, want[idx])
+
+
 def test_small_batch_cuda_core_kernels(networks_golden, monkeypatch):
     """With the tensor-core threshold raised, dense and Input8 stages at small
     batch run the packed-weight GEMV / bit-plane POPC kernels; they must give
