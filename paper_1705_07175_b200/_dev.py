@@ -86,6 +86,21 @@ def sync():
     torch.cuda.current_stream().synchronize()
 
 
+def widen_f4(words: torch.Tensor, rows: int, k: int) -> torch.Tensor:
+    """Packed +/-1 rows (rows, wpl) on the device -> e2m1 nibbles (rows,
+    kpad/2) uint8 for the fp4 tensor-core GEMM (b2_expand_f4)."""
+    kpad = int(_lib.raw("b2_f4_kpad")(int(k)))
+    out = torch.empty((int(rows), kpad // 2), dtype=torch.uint8, device=words.device)
+    wpl = (int(k) + 63) // 64
+    _lib.call("b2_expand_f4", P(words), int(rows), wpl, int(k), P(out), stream())
+    return out
+
+
+def tc_weights(words: torch.Tensor, rows: int, k: int, fmt: str | None = None) -> torch.Tensor:
+    """Tensor-core weights of packed rows in format `fmt` (default _lib.TC_FORMAT)."""
+    return widen_f4(words, rows, k) if (fmt or _lib.TC_FORMAT) == "f4" else widen_i8(words, rows, k)
+
+
 def widen_i8(words: torch.Tensor, rows: int, k: int, permute: bool = True) -> torch.Tensor:
     """Packed +/-1 rows (rows, wpl) on the device -> int8 (rows, kpad) for the
     tensor-core GEMM (b2_expand_i8)."""

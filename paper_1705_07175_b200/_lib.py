@@ -71,7 +71,12 @@ SIGNATURES = {
     "b2_tc_byte_conv_scratch_bytes": (i64, [i64, cint, cint, cint, cint, cint, cint, cint]),
     "b2_tc_byte_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, Thresh, vp, i64, cint, cint, cint, cint, cint,
                                        Thresh, vp, vp, vp]),
+    "b2_f4_kpad": (i64, [i64]),
+    "b2_expand_f4": (cint, [vp, i64, i64, i64, vp, vp]),
 }
+# fp4-weight twins of the tensor-core entry points (same arguments)
+for _n in ("bgemm", "dense_bn_pack", "dense_affine_f64", "conv_forward", "conv_bn_pack", "byte_conv_bn_pack"):
+    SIGNATURES["b2_tc4_" + _n] = SIGNATURES["b2_tc_" + _n]
 
 # GEMM engine for the shapes both engines support: "tc" (tcgen05 int8 tensor
 # cores, the default) or "popc" (LOP3+POPC on the CUDA cores).  The choice
@@ -80,6 +85,19 @@ SIGNATURES = {
 ENGINE = os.environ.get("B2_ENGINE", "tc")
 if ENGINE not in ("tc", "popc"):  # pragma: no cover
     raise ValueError(f"B2_ENGINE must be 'tc' or 'popc', got {ENGINE!r}")
+
+# Tensor-core operand format: "f4" (tcgen05 kind::mxf4, packed e2m1 +/-1
+# with unit block scales: twice the int8 MMA rate and half the operand
+# bytes; the default) or "i8" (kind::i8).  u8-input layers always use i8.
+TC_FORMAT = os.environ.get("B2_TC_FORMAT", "f4")
+if TC_FORMAT not in ("f4", "i8"):  # pragma: no cover
+    raise ValueError(f"B2_TC_FORMAT must be 'f4' or 'i8', got {TC_FORMAT!r}")
+
+
+def tc_entry(op: str, fmt: str | None = None) -> str:
+    """C entry point of tensor-core op `op` for weight format `fmt`."""
+    return ("b2_tc4_" if (fmt or TC_FORMAT) == "f4" else "b2_tc_") + op
+
 
 for _name, (_res, _args) in SIGNATURES.items():
     _fn = getattr(_so, _name)

@@ -27,6 +27,9 @@
 #ifndef B2_BYTES_BN128  // Input8 (u8 rows) on 128-column tiles
 #define B2_BYTES_BN128 0
 #endif
+#ifndef B2_NEPI_F4_128  // epilogue warps of fp4 128-column dense tiles (MMAs twice as fast: drain faster)
+#define B2_NEPI_F4_128 8
+#endif
 #ifndef B2_NEPI_BYTECONV  // epilogue warps of the first conv (one K block per tile)
 #define B2_NEPI_BYTECONV 8
 #endif
@@ -58,6 +61,28 @@ __global__ void k_expand_i8(const uint64_t* __restrict__ w, int64_t rows, int64_
     word |= b << (8 * j);
   }
   reinterpret_cast<uint32_t*>(out)[t] = word;
+}
+
+// Weights for the fp4 path (kind::mxf4): out[r] = kpad/2 bytes of e2m1
+// nibbles, +1.0 (0x2) / -1.0 (0xA) for the bits of K, 0 beyond; 16 bytes
+// per 32-element group in the A side's permuted order (widen_f4m).  One
+// thread per output word.
+__global__ void k_expand_f4(const uint64_t* __restrict__ w, int64_t rows, int64_t wpl, int64_t k, int64_t kpad,
+                            uint32_t* __restrict__ out) {
+  pdl_entry();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per_row = kpad / 8;  // output words
+  if (t >= rows * per_row) return;
+  const int64_t r = t / per_row, o = t - r * per_row;
+  const int64_t j = o >> 2;  // 32-element group
+  const int q = (int)(o & 3);
+  uint32_t x = 0, valid = 0;
+  const int64_t rem = k - 32 * j;
+  if (rem > 0) {
+    x = (uint32_t)(w[r * wpl + (j >> 1)] >> (32 * (j & 1)));
+    valid = rem >= 32 ? ~0u : ((1u << rem) - 1u);
+  }
+  out[t] = (0xAAAAAAAAu ^ ((x << (3 - q)) & 0x88888888u)) & (((valid >> q) & 0x11111111u) * 0xFu);
 }
 
 // network.py:128-138 _PackedByteBN on the raw image followed by the bit
@@ -206,17 +231,17 @@ static int num_sms() {
 
 // KS: split-K over thread-block clusters of g.ksplit CTAs (one tile's K
 // splits), one work item per CTA.
-template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4), bool KS = false>
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4), bool KS = false, bool F4 = false>
 int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st) {
   g.nkb = (int)((k + BKS - 1) / BKS);
-  g.klast = (int)(((k - 1) % BKS) / 32 + 1);
+  g.klast = (int)(((k - 1) % BKS) / (F4 ? 64 : 32) + 1);
   // one N tile whose every K stage fits the B ring space: keep it resident
-  g.resb = (!KS && g.N <= BN && (int64_t)g.nkb * BN * BKS <= (int64_t)b_stages<BN, BKS>() * BN * BKS &&
-            B2_RESIDENT_B) ? 1 : 0;
+  const int b_room = F4 ? f4_stages<BN, BKS>() : b_stages<BN, BKS>();
+  g.resb = (!KS && g.N <= BN && g.nkb <= b_room && B2_RESIDENT_B) ? 1 : 0;
   CUtensorMap map;
-  if (int rc = make_bmap(&map, b_i8, g.N, kpad, BN)) return rc;
-  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS>;
-  constexpr int smem = smem_bytes<BN, AM, BKS>();
+  if (int rc = make_bmap(&map, b_i8, g.N, F4 ? kpad / 2 : kpad, BN)) return rc;
+  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4>;
+  constexpr int smem = smem_bytes<BN, AM, BKS, F4>();
   static std::atomic<uint64_t> attr{0};
   smem_optin(kern, smem, attr);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
@@ -262,9 +287,50 @@ int splitk_count(const Args& g, int64_t k) {
 // tiles (one M=128 x N=256 MMA per 32 K: half the A widening per MAC) with
 // 128-element stages.  Two producer warps per TMEM lane quarter, one for the
 // first conv.
+// fp4 operands (kind::mxf4, both from shared memory): 256-column tiles with
+// 256-element stages (4 K=64 MMAs of 128 cycles), 128-column tiles with
+// 512-element stages (8 of 64 cycles), three accumulator buffers; C = 64
+// convolutions take 16 producer warps (two words per thread: a site is two
+// words).
 template <int AM, int EM>
+int launch_f4(Args g, const int8_t* b, int64_t kpad, cudaStream_t st, int64_t k) {
+  if constexpr (AM == A_BYTES) {
+    return B2_EINVAL;
+  } else {
+    const bool two_words = AM == A_CONV && g.spw % 4 != 0;
+    if (!two_words) {
+      if (int ks = splitk_count<AM, EM>(g, k)) {
+        if constexpr ((EM == E_PACK || EM == E_POOLPACK) && (AM == A_ROWS || AM == A_CONV)) {
+          g.ksplit = ks;
+          return launch_bn<128, AM, EM, 8, 512, 4, true, true>(g, b, kpad, k, st);
+        }
+      }
+    }
+    if constexpr (AM == A_BYTECONV) {
+      return launch_bn<128, AM, EM, 8, 256, B2_NEPI_BYTECONV, false, true>(g, b, kpad, k, st);
+    } else {
+      if constexpr (AM == A_CONV) {
+        if (two_words) {
+          if (g.N > 128) return launch_bn<256, AM, EM, 16, 256, 8, false, true>(g, b, kpad, k, st);
+          return launch_bn<128, AM, EM, 16, 256, 4, false, true>(g, b, kpad, k, st);
+        }
+      }
+      if (g.N > 128) {
+        const int64_t tiles256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
+        if (B2_SMALLM_TILES && tiles256 < B2_SMALLM_TILES)
+          return launch_bn<128, AM, EM, 8, 512, 4, false, true>(g, b, kpad, k, st);
+        return launch_bn<256, AM, EM, 8, 256, 8, false, true>(g, b, kpad, k, st);
+      }
+      if constexpr (AM == A_ROWS) return launch_bn<128, AM, EM, 8, 512, B2_NEPI_F4_128, false, true>(g, b, kpad, k, st);
+      return launch_bn<128, AM, EM, 8, 512, 4, false, true>(g, b, kpad, k, st);
+    }
+  }
+}
+
+template <int AM, int EM, bool F4 = false>
 int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k) {
   if (g.M == 0 || g.N == 0) return 0;
+  if constexpr (F4) return launch_f4<AM, EM>(g, b_i8, kpad, st, k);
   if (int ks = splitk_count<AM, EM>(g, k)) {
     if constexpr ((EM == E_PACK || EM == E_POOLPACK) && (AM == A_ROWS || AM == A_CONV)) {
       g.ksplit = ks;
@@ -297,6 +363,10 @@ int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k)
 }
 
 inline int64_t kpad_of(int64_t k) { return (k + KPAD - 1) / KPAD * KPAD; }
+constexpr int KPAD_F4 = 1024;  // fp4 weight rows: a multiple of the widest stage (512-byte rows)
+inline int64_t kpad_f4(int64_t k) { return (k + KPAD_F4 - 1) / KPAD_F4 * KPAD_F4; }
+template <bool F4>
+inline int64_t kpad_for(int64_t k) { return F4 ? kpad_f4(k) : kpad_of(k); }
 static_assert(KPAD % 128 == 0, "weight rows pad to whole TMA boxes");
 
 inline bool conv_ok(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad) {
@@ -319,6 +389,9 @@ inline void conv_args(Args& g, const void* x, int64_t batch, int h, int w, int c
   g.Ho = (h + 2 * pad - kh) / stride + 1;
   g.Wo = (w + 2 * pad - kw) / stride + 1;
   g.M = batch * g.Ho * g.Wo;
+  // exact for dividends below 2^32 / divisor (K words and window cells here)
+  g.spw_magic = ((1ull << 32) + (uint64_t)(g.spw > 0 ? g.spw : 1) - 1) / (uint64_t)(g.spw > 0 ? g.spw : 1);
+  g.kw_magic = ((1ull << 32) + (uint64_t)kw - 1) / (uint64_t)kw;
 }
 
 inline void pack_args(Args& g, const b2_thresh& th, uint64_t* out, int64_t n) {
@@ -326,6 +399,120 @@ inline void pack_args(Args& g, const b2_thresh& th, uint64_t* out, int64_t n) {
   g.ldo32 = 2 * wpl64(n);
   g.thresh = th.thresh;
   g.ge = th.ge_dir;
+}
+
+template <bool F4>
+int bgemm(const uint64_t* a, int64_t m, const int8_t* b_i8, int64_t n, int64_t wpl, int32_t k, int32_t* out,
+                void* stream) {
+  if (m < 0 || n < 0 || wpl < 1 || k < 1 || k > 64 * wpl || n > INT32_MAX) return B2_EINVAL;
+  Args g{};
+  g.a = reinterpret_cast<const uint32_t*>(a);
+  g.lda = 2 * wpl;
+  g.awords = (k + 31) / 32;
+  g.M = m;
+  g.N = (int)n;
+  g.out_i32 = out;
+  g.ldo = n;
+  return launch<A_ROWS, E_I32, F4>(g, b_i8, kpad_for<F4>(k), S(stream), k);
+}
+
+template <bool F4>
+int dense_affine_f64(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl,
+                           int32_t k, const double* mean, const double* scale, const double* beta, double* out,
+                           void* stream) {
+  if (units < 1 || units > INT32_MAX || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl || !mean || !scale || !beta)
+    return B2_EINVAL;
+  Args g{};
+  g.a = reinterpret_cast<const uint32_t*>(x);
+  g.lda = 2 * wpl;
+  g.awords = (k + 31) / 32;
+  g.M = batch;
+  g.N = (int)units;
+  g.mean = mean;
+  g.scale = scale;
+  g.beta = beta;
+  g.out_f64 = out;
+  g.ldo = units;
+  return launch<A_ROWS, E_AFFINE, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
+}
+
+template <bool F4>
+int dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl, int32_t k,
+                        b2_thresh th, uint64_t* out, void* stream) {
+  if (units < 1 || units > INT32_MAX || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl || !th.thresh || !th.ge_dir)
+    return B2_EINVAL;
+  Args g{};
+  g.a = reinterpret_cast<const uint32_t*>(x);
+  g.lda = 2 * wpl;
+  g.awords = (k + 31) / 32;
+  g.M = batch;
+  g.N = (int)units;
+  pack_args(g, th, out, units);
+  return launch<A_ROWS, E_PACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
+}
+
+template <bool F4>
+int conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
+                       int64_t filters, int kh, int kw, int stride, int pad, int32_t* out, void* stream) {
+  if (!conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || c % 64) return B2_EINVAL;
+  Args g{};
+  conv_args(g, lines, batch, h, w, c, kh, kw, stride, pad);
+  const int64_t k = (int64_t)kh * kw * c;
+  g.N = (int)filters;
+  g.out_i32 = out;
+  g.ldo = filters;
+  return launch<A_CONV, E_I32, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
+}
+
+template <bool F4>
+int conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
+                       int64_t filters, int kh, int kw, int stride, int pad, int pool, b2_thresh th, uint64_t* out,
+                       void* stream) {
+  if (!conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || c % 64 || !th.thresh || !th.ge_dir)
+    return B2_EINVAL;
+  Args g{};
+  conv_args(g, lines, batch, h, w, c, kh, kw, stride, pad);
+  if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
+  const int64_t k = (int64_t)kh * kw * c;
+  g.N = (int)filters;
+  pack_args(g, th, out, filters);
+  if (pool) return launch<A_CONV, E_POOLPACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
+  return launch<A_CONV, E_PACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
+}
+
+template <bool F4>
+int byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
+                            const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
+                            b2_thresh th_out, void* scratch, uint64_t* out, void* stream) {
+  if (!conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > BK || c > 8 || !scratch ||
+      !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir)
+    return B2_EINVAL;
+  Args g{};
+  conv_args(g, x, batch, h, w, c, kh, kw, stride, pad);
+  if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
+  if (!batch) return 0;
+  const int64_t k = (int64_t)kh * kw * c;
+  const int kw32 = (int)((k + 31) / 32);
+  {
+    const int bands = (g.Ho + BAND - 1) / BAND;
+    const int in_rows = (BAND - 1) * stride + kh;
+    const size_t smem = (size_t)in_rows * w;
+    if (smem > 48 * 1024 || batch * bands > INT32_MAX) return B2_EINVAL;
+    auto kern = (kh == 3 && kw == 3 && c == 3) ? k_byte_unroll<3, 3, 3> : k_byte_unroll<0, 0, 0>;
+    launch_k(kern, (unsigned)(batch * bands), 256, smem, S(stream), 
+        x, h, w, c, kh, kw, stride, pad, g.Ho, g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
+        reinterpret_cast<uint32_t*>(scratch));
+  }
+  if (int rc = launched()) return rc;
+  // rows are ordered like the conv output (pool-window-major when pooled)
+  g.a = reinterpret_cast<const uint32_t*>(scratch);
+  g.lda = 2 * kw32;
+  g.awords = kw32;
+  g.N = (int)filters;
+  g.nkb = 1;
+  pack_args(g, th_out, out, filters);
+  if (pool) return launch<A_BYTECONV, E_POOLPACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
+  return launch<A_BYTECONV, E_PACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
 }
 
 }  // namespace tc
@@ -346,79 +533,48 @@ int b2_expand_i8(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, int pe
   return launched();
 }
 
-int b2_tc_bgemm(const uint64_t* a, int64_t m, const int8_t* b_i8, int64_t n, int64_t wpl, int32_t k, int32_t* out,
-                void* stream) {
-  if (m < 0 || n < 0 || wpl < 1 || k < 1 || k > 64 * wpl || n > INT32_MAX) return B2_EINVAL;
-  tc::Args g{};
-  g.a = reinterpret_cast<const uint32_t*>(a);
-  g.lda = 2 * wpl;
-  g.awords = (k + 31) / 32;
-  g.M = m;
-  g.N = (int)n;
-  g.out_i32 = out;
-  g.ldo = n;
-  return tc::launch<tc::A_ROWS, tc::E_I32>(g, b_i8, tc::kpad_of(k), S(stream), k);
+int64_t b2_f4_kpad(int64_t k) { return tc::kpad_f4(k); }
+
+int b2_expand_f4(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, uint8_t* out, void* stream) {
+  if (rows < 0 || wpl < 1 || k < 1 || k > 64 * wpl) return B2_EINVAL;
+  const int64_t kpad = tc::kpad_f4(k);
+  const int64_t n = rows * kpad / 8;
+  if (!n) return 0;
+  launch_k(tc::k_expand_f4, (unsigned)cdiv(n, 256), 256, 0, S(stream), w, rows, wpl, k, kpad,
+           reinterpret_cast<uint32_t*>(out));
+  return launched();
 }
 
-int b2_tc_dense_affine_f64(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl,
-                           int32_t k, const double* mean, const double* scale, const double* beta, double* out,
-                           void* stream) {
-  if (units < 1 || units > INT32_MAX || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl || !mean || !scale || !beta)
-    return B2_EINVAL;
-  tc::Args g{};
-  g.a = reinterpret_cast<const uint32_t*>(x);
-  g.lda = 2 * wpl;
-  g.awords = (k + 31) / 32;
-  g.M = batch;
-  g.N = (int)units;
-  g.mean = mean;
-  g.scale = scale;
-  g.beta = beta;
-  g.out_f64 = out;
-  g.ldo = units;
-  return tc::launch<tc::A_ROWS, tc::E_AFFINE>(g, w_i8, tc::kpad_of(k), S(stream), k);
-}
+#define B2_TC_WRAP(NAME, IMPL, PARAMS, ARGS)                              \
+  int b2_tc_##NAME PARAMS { return tc::IMPL<false> ARGS; }                \
+  int b2_tc4_##NAME PARAMS { return tc::IMPL<true> ARGS; }
 
-int b2_tc_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_i8, int64_t units, int64_t wpl, int32_t k,
-                        b2_thresh th, uint64_t* out, void* stream) {
-  if (units < 1 || units > INT32_MAX || batch < 0 || wpl < 1 || k < 1 || k > 64 * wpl || !th.thresh || !th.ge_dir)
-    return B2_EINVAL;
-  tc::Args g{};
-  g.a = reinterpret_cast<const uint32_t*>(x);
-  g.lda = 2 * wpl;
-  g.awords = (k + 31) / 32;
-  g.M = batch;
-  g.N = (int)units;
-  tc::pack_args(g, th, out, units);
-  return tc::launch<tc::A_ROWS, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
-}
-
-int b2_tc_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
-                       int64_t filters, int kh, int kw, int stride, int pad, int32_t* out, void* stream) {
-  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || c % 64) return B2_EINVAL;
-  tc::Args g{};
-  tc::conv_args(g, lines, batch, h, w, c, kh, kw, stride, pad);
-  const int64_t k = (int64_t)kh * kw * c;
-  g.N = (int)filters;
-  g.out_i32 = out;
-  g.ldo = filters;
-  return tc::launch<tc::A_CONV, tc::E_I32>(g, w_i8, tc::kpad_of(k), S(stream), k);
-}
-
-int b2_tc_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_i8,
-                       int64_t filters, int kh, int kw, int stride, int pad, int pool, b2_thresh th, uint64_t* out,
-                       void* stream) {
-  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || c % 64 || !th.thresh || !th.ge_dir)
-    return B2_EINVAL;
-  tc::Args g{};
-  tc::conv_args(g, lines, batch, h, w, c, kh, kw, stride, pad);
-  if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
-  const int64_t k = (int64_t)kh * kw * c;
-  g.N = (int)filters;
-  tc::pack_args(g, th, out, filters);
-  if (pool) return tc::launch<tc::A_CONV, tc::E_POOLPACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
-  return tc::launch<tc::A_CONV, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
-}
+B2_TC_WRAP(bgemm, bgemm,
+           (const uint64_t* a, int64_t m, const int8_t* b, int64_t n, int64_t wpl, int32_t k, int32_t* out,
+            void* stream),
+           (a, m, b, n, wpl, k, out, stream))
+B2_TC_WRAP(dense_affine_f64, dense_affine_f64,
+           (const uint64_t* x, int64_t batch, const int8_t* w, int64_t units, int64_t wpl, int32_t k,
+            const double* mean, const double* scale, const double* beta, double* out, void* stream),
+           (x, batch, w, units, wpl, k, mean, scale, beta, out, stream))
+B2_TC_WRAP(dense_bn_pack, dense_bn_pack,
+           (const uint64_t* x, int64_t batch, const int8_t* w, int64_t units, int64_t wpl, int32_t k, b2_thresh th,
+            uint64_t* out, void* stream),
+           (x, batch, w, units, wpl, k, th, out, stream))
+B2_TC_WRAP(conv_forward, conv_forward,
+           (const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* wt, int64_t filters, int kh,
+            int kw, int stride, int pad, int32_t* out, void* stream),
+           (lines, batch, h, w, c, wt, filters, kh, kw, stride, pad, out, stream))
+B2_TC_WRAP(conv_bn_pack, conv_bn_pack,
+           (const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* wt, int64_t filters, int kh,
+            int kw, int stride, int pad, int pool, b2_thresh th, uint64_t* out, void* stream),
+           (lines, batch, h, w, c, wt, filters, kh, kw, stride, pad, pool, th, out, stream))
+B2_TC_WRAP(byte_conv_bn_pack, byte_conv_bn_pack,
+           (const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in, const int8_t* wt,
+            int64_t filters, int kh, int kw, int stride, int pad, int pool, b2_thresh th_out, void* scratch,
+            uint64_t* out, void* stream),
+           (x, batch, h, w, c, th_in, wt, filters, kh, kw, stride, pad, pool, th_out, scratch, out, stream))
+#undef B2_TC_WRAP
 
 int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_t* w_i8, int64_t units, b2_thresh th,
                          uint64_t* out, void* stream) {
@@ -438,40 +594,6 @@ int64_t b2_tc_byte_conv_scratch_bytes(int64_t batch, int h, int w, int c, int kh
   const int64_t ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
   const int64_t kw32 = ((int64_t)kh * kw * c + 31) / 32;
   return batch * ho * wo * 2 * kw32 * 4;
-}
-
-int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
-                            const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
-                            b2_thresh th_out, void* scratch, uint64_t* out, void* stream) {
-  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || (int64_t)kh * kw * c > tc::BK || c > 8 || !scratch ||
-      !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir)
-    return B2_EINVAL;
-  tc::Args g{};
-  tc::conv_args(g, x, batch, h, w, c, kh, kw, stride, pad);
-  if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
-  if (!batch) return 0;
-  const int64_t k = (int64_t)kh * kw * c;
-  const int kw32 = (int)((k + 31) / 32);
-  {
-    const int bands = (g.Ho + tc::BAND - 1) / tc::BAND;
-    const int in_rows = (tc::BAND - 1) * stride + kh;
-    const size_t smem = (size_t)in_rows * w;
-    if (smem > 48 * 1024 || batch * bands > INT32_MAX) return B2_EINVAL;
-    auto kern = (kh == 3 && kw == 3 && c == 3) ? tc::k_byte_unroll<3, 3, 3> : tc::k_byte_unroll<0, 0, 0>;
-    launch_k(kern, (unsigned)(batch * bands), 256, smem, S(stream), 
-        x, h, w, c, kh, kw, stride, pad, g.Ho, g.Wo, kw32, pool, th_in.thresh, th_in.ge_dir,
-        reinterpret_cast<uint32_t*>(scratch));
-  }
-  if (int rc = launched()) return rc;
-  // rows are ordered like the conv output (pool-window-major when pooled)
-  g.a = reinterpret_cast<const uint32_t*>(scratch);
-  g.lda = 2 * kw32;
-  g.awords = kw32;
-  g.N = (int)filters;
-  g.nkb = 1;
-  tc::pack_args(g, th_out, out, filters);
-  if (pool) return tc::launch<tc::A_BYTECONV, tc::E_POOLPACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
-  return tc::launch<tc::A_BYTECONV, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 
 }  // extern "C"

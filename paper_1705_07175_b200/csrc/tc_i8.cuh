@@ -59,6 +59,7 @@ struct Args {
   int awords;         // A_ROWS/A_BYTECONV: valid uint32 words per row (ceil(K/32)); A_BYTES: valid words
   // conv geometry (A_CONV: spw = C/32 words per site; A_BYTECONV: c = channels)
   int H, W, spw, sstride, kh, kw, stride, pad, Ho, Wo, c;
+  uint64_t spw_magic, kw_magic;  // ceil(2^32 / spw), ceil(2^32 / kw): exact division of small operands
   // ---- problem
   int64_t M;
   int N;
@@ -273,11 +274,60 @@ __device__ __forceinline__ void widen32m(uint32_t x, uint32_t valid, uint32_t* o
   for (int q = 0; q < 8; ++q) o[q] = ((nx >> q) & 0x01010101u) * 0xFEu + ((valid >> q) & 0x01010101u);
 }
 
+// ---- fp4 operands (tcgen05.mma kind::mxf4, e2m1 with unit block scales).
+// +1.0 = 0x2, -1.0 = 0xA, 0 = 0x0 are exact in e2m1; products are +/-1 and
+// the fp32 accumulator holds the exact integer dot product (|dot| < 2^24).
+// 32 bits -> 32 nibbles (4 words, 16 bytes): nibble i of word q holds
+// element 4i + q (a common permutation of K within each 32-group, applied to
+// the weights too by k_expand_f4): one shift and one LOP3 per word.
+// Branch-free: with m = all ones for a valid word (else 0), nibble =
+// 0x2 (valid) | 0x8 (valid and bit 0): one LOP3 for ~x & m, then a shift and
+// one LOP3 per output word.
+__device__ __forceinline__ void widen_f4(uint32_t x, bool ok, uint32_t* o) {
+  const uint32_t m = 0u - (uint32_t)ok;
+  const uint32_t nx = ~x & m, c2 = m & 0x22222222u;
+  o[0] = ((nx << 3) & 0x88888888u) | c2;
+  o[1] = ((nx << 2) & 0x88888888u) | c2;
+  o[2] = ((nx << 1) & 0x88888888u) | c2;
+  o[3] = (nx & 0x88888888u) | c2;
+}
+__device__ __forceinline__ void widen_f4m(uint32_t x, uint32_t valid, uint32_t* o) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    o[q] = (0xAAAAAAAAu ^ ((x << (3 - q)) & 0x88888888u)) & (((valid >> q) & 0x11111111u) * 0xFu);
+}
+__host__ __device__ __forceinline__ int perm_pos_f4(int k) {  // element k of a 32-group -> nibble position
+  return 8 * (k & 3) + (k >> 2);
+}
+// instruction descriptor, kind::mxf4: A/B e2m1 (1), both K-major, UE8M0
+// scales, M = 128, K = 64 per instruction (cute InstrDescriptorBlockScaled)
+__host__ __device__ constexpr uint32_t idesc_f4(int n) {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_f4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+          d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {  // generic-proxy smem writes -> tensor-core reads
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Gather cursor of one A-producer thread (one tile row, one half of each
 // 128-element K block): walks this CTA's (tile, K block) sequence.
 //   A_ROWS / A_CONV / A_BYTECONV: 64 packed bits (uint2) + validity
 //   A_BYTES:                      64 raw bytes (4 x uint4)
-template <int AM, bool POOLED, int WS, int TW>  // WS = K words per stage, TW = words per producer thread
+// DIRECT (conv): every chunk's window cell and word are computed from its
+// absolute K word (no incremental cell walk, no branches).
+__device__ __forceinline__ uint32_t div_magic(uint32_t n, uint64_t magic) {  // n / d, n < 2^16, d < 2^16
+  return (uint32_t)(((uint64_t)n * magic) >> 32);
+}
+template <int AM, bool POOLED, int WS, int TW, bool DIRECT = false>  // WS = K words per stage, TW = words per producer thread
 struct ACursor {
   int64_t t;       // work item of the next fetch (tile t / ksp)
   int kb, kend;    // K block of the next fetch, end of the item's K range
@@ -299,9 +349,11 @@ struct ACursor {
       iy0 = oy * g.stride - g.pad;
       ix0 = ox * g.stride - g.pad;
       base = g.a + img * (int64_t)g.H * g.W * g.sstride;
-      cell = dy = dx = 0;
-      within = TW * half + kb * WS;  // this producer warp's first word of the item's first stage
-      while (within >= g.spw) within -= g.spw, step_cell(g);
+      if constexpr (!DIRECT) {
+        cell = dy = dx = 0;
+        within = TW * half + kb * WS;  // this producer warp's first word of the item's first stage
+        while (within >= g.spw) within -= g.spw, step_cell(g);
+      }
     } else {
       base = g.a + (mok ? m : 0) * g.lda;
     }
@@ -320,10 +372,22 @@ struct ACursor {
     if (++kb == kend) {
       t += step;
       tile_setup(g, mtiles, tiles, r, half, ksp);
-    } else if constexpr (AM == A_CONV) {
+    } else if constexpr (AM == A_CONV && !DIRECT) {
       within += WS;
       while (within >= g.spw) within -= g.spw, step_cell(g);
     }
+  }
+
+  // DIRECT conv: address of K word `wpos` of this row's window (site
+  // cell = wpos / spw, word within the site, cell -> (dy, dx)); ok = in bounds
+  __device__ __forceinline__ const uint32_t* conv_word(const Args& g, int wpos, bool& ok) const {
+    const uint32_t cell = div_magic((uint32_t)wpos, g.spw_magic);
+    const int within_ = wpos - (int)cell * g.spw;
+    const uint32_t dy_ = div_magic(cell, g.kw_magic);
+    const int dx_ = (int)cell - (int)dy_ * g.kw;
+    const int iy = iy0 + (int)dy_, ix = ix0 + dx_;
+    ok = mok && (int)dy_ < g.kh && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
+    return base + ((int64_t)iy * g.W + ix) * g.sstride + within_;
   }
 
   // packed-bit modes: x = WPH words (32 bits each) of K starting at word
@@ -348,6 +412,18 @@ struct ACursor {
           if (w0 + 1 < g.awords) x.y = __ldg(p + 1);
           if (WPH == 4 && w0 + 2 < g.awords) x.z = __ldg(p + 2);
           if (WPH == 4 && w0 + 3 < g.awords) x.w = __ldg(p + 3);
+        }
+      }
+    } else if constexpr (AM == A_CONV && DIRECT) {
+      bool ok;
+      const uint32_t* p = conv_word(g, kb * WS + WPH * half, ok);
+      if (ok) {
+        vm = make_uint4(~0u, ~0u, ~0u, ~0u);
+        if constexpr (WPH == 4) {
+          x = __ldg(reinterpret_cast<const uint4*>(p));
+        } else {
+          const uint2 y = __ldg(reinterpret_cast<const uint2*>(p));
+          x.x = y.x, x.y = y.y;
         }
       }
     } else if constexpr (AM == A_CONV) {
@@ -398,6 +474,12 @@ struct ACursor {
             if (w + 3 < g.awords) x[j].w = __ldg(p + 4 * j + 3);
           }
         }
+      }
+    } else if constexpr (AM == A_CONV && DIRECT) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t* p = conv_word(g, kb * WS + 8 * half + 4 * j, ok[j]);
+        if (ok[j]) x[j] = __ldg(reinterpret_cast<const uint4*>(p));
       }
     } else if constexpr (AM == A_CONV) {
       // chunk 0 at the cursor's (cell, within); chunk 1 four words later
@@ -500,6 +582,18 @@ template <int BN, int BKS>
 constexpr int b_stages() {  // 192 KB of shared memory for the B ring
   return (192 * 1024) / (BN * BKS);
 }
+// fp4 (kind::mxf4): A and B stages both in shared memory, 4 bits per
+// element; the ring holds f4_stages() of each in 192 KB.  TMEM holds only
+// accumulators (3 x 128 or 1 x 256 columns) and the unit scale factors.
+template <int BN, int BKS>
+constexpr int f4_stages() {
+  return (192 * 1024) / ((BN + BM) * BKS / 2);
+}
+template <int BN>
+constexpr int f4_acc_bufs() {
+  return BN > 128 ? 1 : 3;
+}
+constexpr int F4_SF_COLS = 16;  // TMEM columns of 0x7F (2^0) scale bytes, after the accumulators
 
 template <int NEPI>
 __device__ __forceinline__ void epi_bar() {  // named barrier of the epilogue warps
@@ -512,6 +606,7 @@ constexpr int THR_COLS = 2048;  // resident threshold table (columns)
 // by the nthr epilogue threads (et = 0 .. nthr-1): ge -> (1, -t), le ->
 // (-1, t), column beyond N -> (0, -1) = bit 0; one ge-direction mask word
 // per 32 columns (ballot).
+template <bool F4 = false>
 __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncols, int et, int nthr, int lane,
                                                  int4* sthr, uint32_t* sgm) {
   int* st = reinterpret_cast<int*>(sthr);
@@ -525,8 +620,13 @@ __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncol
       mul = ge ? 1 : -1;
       add = ge ? -th : th;
     }
-    st[2 * j] = mul;
-    st[2 * j + 1] = add;
+    if constexpr (F4) {  // fp32 accumulators: (mul, add) as floats (|add| < 2^24 exact; larger only for sentinels)
+      st[2 * j] = __float_as_int((float)mul);
+      st[2 * j + 1] = __float_as_int((float)add);
+    } else {
+      st[2 * j] = mul;
+      st[2 * j + 1] = add;
+    }
     const uint32_t gmw = __ballot_sync(0xffffffffu, ge);
     if (lane == 0) sgm[j >> 5] = gmw;
   }
@@ -534,17 +634,33 @@ __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncol
 
 // Packed sign word of 32 accumulators: bit j = (v[j] * mul_j + add_j >= 0)
 // with trow = the columns' (mul, add) pairs (sign bits MSB first, reversed).
+// F4: v holds fp32 accumulators and the table float (mul, add); the sign of
+// the exact fma is the sign of the integer form.
+template <bool F4 = false>
 __device__ __forceinline__ uint32_t thr_word(const uint32_t (&v)[32], const int4* trow) {
   uint32_t sg = 0;
 #pragma unroll
   for (int j = 0; j < 32; j += 2) {
     const int4 p = trow[j / 2];
-    const int d0 = (int)v[j] * p.x + p.y;
-    const int d1 = (int)v[j + 1] * p.z + p.w;
-    sg = __funnelshift_l((uint32_t)d0, sg, 1);
-    sg = __funnelshift_l((uint32_t)d1, sg, 1);
+    uint32_t d0, d1;
+    if constexpr (F4) {
+      d0 = __float_as_uint(fmaf(__uint_as_float(v[j]), __int_as_float(p.x), __int_as_float(p.y)));
+      d1 = __float_as_uint(fmaf(__uint_as_float(v[j + 1]), __int_as_float(p.z), __int_as_float(p.w)));
+    } else {
+      d0 = (uint32_t)((int)v[j] * p.x + p.y);
+      d1 = (uint32_t)((int)v[j + 1] * p.z + p.w);
+    }
+    sg = __funnelshift_l(d0, sg, 1);
+    sg = __funnelshift_l(d1, sg, 1);
   }
   return ~__brev(sg);
+}
+template <bool F4>
+__device__ __forceinline__ int acc_int(uint32_t v) {  // accumulator -> exact integer
+  if constexpr (F4)
+    return __float2int_rn(__uint_as_float(v));
+  else
+    return (int)v;
 }
 // 2x2 max-pool of thresholded rows held by 4 consecutive lanes: max then
 // threshold == OR (ge columns, mask gm) / AND (le) of the four words
@@ -569,7 +685,7 @@ constexpr int num_threads() {
 // quarter, half the columns each: TMEM reads are latency-bound per warp,
 // ~42 B/clk each, so a single-buffered 256-column accumulator drains twice
 // as fast).
-template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS>
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4>
 __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
                                                                   const Args g) {
   constexpr int WS = BKS / 32;        // K words per stage
@@ -579,26 +695,34 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   constexpr int EPI0 = 4 + NPW;       // first epilogue warp
   static_assert(WPH == 2 || WPH == 4 || WPH == 8, "producer word split");
   constexpr bool POOLED = (EM == E_POOLPACK);
-  constexpr int B_STAGE_BYTES = BN * BKS;
+  static_assert(!F4 || AM != A_BYTES, "u8 rows are not fp4 operands");
+  constexpr int B_STAGE_BYTES = F4 ? BN * BKS / 2 : BN * BKS;
+  constexpr int A_STAGE_BYTES = BM * BKS / 2;  // fp4: A stage in shared memory
+  constexpr int KMMA = F4 ? 64 : 32;            // K per MMA instruction
+  constexpr int VW = F4 ? 4 : 8;                // widened words per 32-bit input word
   // one ring: stage s = B tile in shared memory + A block in TMEM, one
   // full barrier (TMA bytes + producer warps) and one empty barrier (MMA
   // commit): the issuing thread's per-stage waits and commits are serial
   // time the tensor pipe cannot hide at N = 128 (tools/microbench/mma_loop.cu)
-  constexpr int SA = a_stages<BN, AM, BKS>() < b_stages<BN, BKS>() ? a_stages<BN, AM, BKS>() : b_stages<BN, BKS>();
+  constexpr int SA = F4 ? f4_stages<BN, BKS>()
+                       : (a_stages<BN, AM, BKS>() < b_stages<BN, BKS>() ? a_stages<BN, AM, BKS>() : b_stages<BN, BKS>());
   constexpr int SB = SA;
   constexpr int ACC_COLS = BN;
-  constexpr int ACC_BUFS = acc_bufs<BN, AM>();
-  constexpr int A_COL0 = ACC_BUFS * ACC_COLS;
-  static_assert(A_COL0 + SA * A_STAGE_COLS <= 512, "TMEM budget");
-  constexpr uint32_t IDESC = idesc_i8(BN, AM == A_BYTES);
+  constexpr int ACC_BUFS = F4 ? f4_acc_bufs<BN>() : acc_bufs<BN, AM>();
+  constexpr int A_COL0 = ACC_BUFS * ACC_COLS;  // i8: A ring; fp4: scale-factor columns
+  static_assert(F4 ? (A_COL0 + F4_SF_COLS <= 512) : (A_COL0 + SA * A_STAGE_COLS <= 512), "TMEM budget");
+  constexpr uint32_t IDESC = F4 ? idesc_f4(BN) : idesc_i8(BN, AM == A_BYTES);
+  constexpr int B_REGION = F4 ? SB * B_STAGE_BYTES : b_stages<BN, BKS>() * B_STAGE_BYTES;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the shared array (an
   // integer round trip would turn every table read into a generic load)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sb = smem;                                                      // SB x B_STAGE_BYTES
-  // the B region is sized for b_stages() (a resident B tile may use all of it)
-  int4* sthr = reinterpret_cast<int4*>(smem + b_stages<BN, BKS>() * B_STAGE_BYTES);  // THR_COLS/2 x (mul, add, ...)
+  // the B region is sized for b_stages() (a resident B tile may use all of it);
+  // fp4: the A ring follows it
+  uint8_t* sa = smem + B_REGION;
+  int4* sthr = reinterpret_cast<int4*>(smem + B_REGION + (F4 ? SA * A_STAGE_BYTES : 0));  // THR_COLS/2 x (mul, add, ...)
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + THR_COLS / 2);        // THR_COLS/32 ge-direction masks
   uint64_t* full = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
   uint64_t* empty = full + SA;
@@ -638,6 +762,18 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (F4) {  // unit block scales (e8m0 0x7F = 2^0) for A and B, every lane
+    if (warp < 4) {
+      uint32_t ones[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) ones[i] = 0x7F7F7F7Fu;
+      tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + A_COL0, ones);
+      tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   // barriers, TMEM and the tensor map are set up while the previous kernel
   // drains; every global access (weights included: a widen may have just
   // written them) comes after the wait
@@ -656,8 +792,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         mbar_expect_tx(bres, (uint32_t)g.nkb * B_STAGE_BYTES);
         for (int kb = 0; kb < g.nkb; ++kb)
 #pragma unroll
-          for (int at = 0; at < BKS / BK; ++at)
-            tma_load_2d(sb + kb * B_STAGE_BYTES + at * BN * BK, &bmap, bres, kb * BKS + at * BK, 0);
+          for (int at = 0; at < (F4 ? BKS / 256 : BKS / BK); ++at)
+            tma_load_2d(sb + kb * B_STAGE_BYTES + at * BN * BK, &bmap, bres, (F4 ? kb * BKS / 2 : kb * BKS) + at * BK, 0);
       }
       for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
         const int n0 = (int)(t / ksp / mtiles) * BN;
@@ -670,8 +806,9 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], B_STAGE_BYTES);
 #pragma unroll
-          for (int at = 0; at < BKS / BK; ++at)  // one 128-byte-wide box per swizzle atom
-            tma_load_2d(sb + s * B_STAGE_BYTES + at * BN * BK, &bmap, &full[s], kb * BKS + at * BK, n0);
+          for (int at = 0; at < (F4 ? BKS / 256 : BKS / BK); ++at)  // one 128-byte-wide box per swizzle atom
+            tma_load_2d(sb + s * B_STAGE_BYTES + at * BN * BK, &bmap, &full[s], (F4 ? kb * BKS / 2 : kb * BKS) + at * BK,
+                        n0);
           if (++s == SB) s = 0, ph ^= 1;
         }
       }
@@ -693,14 +830,25 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
           const uint32_t bs = smem_u32(sb + (resb ? kb : s) * B_STAGE_BYTES);
-          const int kmma = kb + 1 == g.nkb ? g.klast : BKS / 32;
+          const int kmma = kb + 1 == g.nkb ? g.klast : BKS / KMMA;
+          if constexpr (F4) {
+            // both operands in shared memory: 4 K=64 MMAs per 128-byte swizzle atom
+            const uint32_t as = smem_u32(sa + s * A_STAGE_BYTES);
 #pragma unroll
-          for (int k = 0; k < BKS / 32; ++k)
-            if (k < kmma)
-              tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC,
-                        (kb > kb0 || k) ? 1u : 0u);
+            for (int k = 0; k < BKS / 64; ++k)
+              if (k < kmma)
+                tc_mma_f4(d, sw128_desc(as + (k >> 2) * BM * BK + (k & 3) * 32),
+                          sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, tmem + A_COL0,
+                          tmem + A_COL0 + 4, (kb > kb0 || k) ? 1u : 0u);
+          } else {
+            const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
+#pragma unroll
+            for (int k = 0; k < BKS / 32; ++k)
+              if (k < kmma)
+                tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC,
+                          (kb > kb0 || k) ? 1u : 0u);
+          }
           tc_commit(&empty[s]);
           if (++s == SA) s = 0, ph ^= 1;
         }
@@ -719,7 +867,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     const int half = HALVES == 1 ? 0 : (warp - 4) >> 2;
     const int r = q * 32 + lane;  // tile row = TMEM lane
     const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / HALVES);
-    ACursor<AM, POOLED, WS, WPH> cur;
+    ACursor<AM, POOLED, WS, WPH, F4 && AM == A_CONV> cur;
     cur.start(g, blockIdx.x, mtiles, tiles, r, half, ksp);
     int64_t jobs;
     if constexpr (KS) {
@@ -738,7 +886,27 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     // every stage feeds exactly one K=32 MMA (K <= 32, one stage): the first
     // conv; only the first word of each producer's share is consumed
     const bool short_k = HALVES == 1 && g.nkb == 1 && g.klast == 1;
-    auto publish = [&](int stage, uint32_t (&v)[8 * WPH]) {  // WPH 2/4/8 -> 16/32/64 TMEM columns
+    auto publish = [&](int stage, uint32_t (&v)[VW * WPH]) {  // i8: WPH 2/4/8 -> 16/32/64 TMEM columns
+      if constexpr (F4) {
+        // fp4: this thread's WPH words of the stage are WPH 16-byte chunks of
+        // its row in the shared-memory A stage (128-byte swizzle, K-major)
+        mbar_wait(&empty[stage], ph ^ 1);
+        uint8_t* row = sa + stage * A_STAGE_BYTES + r * 128;
+        // one K stage per tile (the first conv): only the words its klast
+        // K=64 MMAs read are stored
+        const int wend = g.nkb == 1 ? 2 * g.klast : WS;
+#pragma unroll
+        for (int i = 0; i < WPH; ++i) {
+          const int w = half * WPH + i;
+          if (w < wend)
+            *reinterpret_cast<uint4*>(row + (w >> 3) * (BM * 128) + (((w & 7) ^ (r & 7)) << 4)) =
+                make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        return;
+      }
       if (pending >= 0) {
         tmem_wait_st();
         tc_fence_before();
@@ -805,14 +973,21 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #pragma unroll
         for (int u = 0; u < PF8; ++u) {
           if (j0 + u < ijobs) {
-            uint32_t v[64];
+            uint32_t v[VW * 8];
 #ifndef B2_PROBE_SKIP_A
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-              widen32(qx[u][c].x, qok[u][c], v + 32 * c + 0);
-              widen32(qx[u][c].y, qok[u][c], v + 32 * c + 8);
-              widen32(qx[u][c].z, qok[u][c], v + 32 * c + 16);
-              widen32(qx[u][c].w, qok[u][c], v + 32 * c + 24);
+              if constexpr (F4) {
+                widen_f4(qx[u][c].x, qok[u][c], v + 16 * c + 0);
+                widen_f4(qx[u][c].y, qok[u][c], v + 16 * c + 4);
+                widen_f4(qx[u][c].z, qok[u][c], v + 16 * c + 8);
+                widen_f4(qx[u][c].w, qok[u][c], v + 16 * c + 12);
+              } else {
+                widen32(qx[u][c].x, qok[u][c], v + 32 * c + 0);
+                widen32(qx[u][c].y, qok[u][c], v + 32 * c + 8);
+                widen32(qx[u][c].z, qok[u][c], v + 32 * c + 16);
+                widen32(qx[u][c].w, qok[u][c], v + 32 * c + 24);
+              }
             }
 #endif
             cur.fetch_bits8(g, half, qx[u], qok[u]);
@@ -841,9 +1016,25 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #pragma unroll
         for (int u = 0; u < PF; ++u) {
           if (j0 + u < ijobs) {
-            uint32_t v[8 * WPH];
+            uint32_t v[VW * WPH];
 #ifndef B2_PROBE_SKIP_A
-            if constexpr (MASKED) {
+            if constexpr (F4) {
+              if constexpr (MASKED) {
+                widen_f4m(qx[u].x, qv[u].x, v + 0);
+                widen_f4m(qx[u].y, qv[u].y, v + 4);
+                if constexpr (WPH == 4) {
+                  widen_f4m(qx[u].z, qv[u].z, v + 8);
+                  widen_f4m(qx[u].w, qv[u].w, v + 12);
+                }
+              } else {
+                widen_f4(qx[u].x, qok[u], v + 0);
+                widen_f4(qx[u].y, qok[u], v + 4);
+                if constexpr (WPH == 4) {
+                  widen_f4(qx[u].z, qok[u], v + 8);
+                  widen_f4(qx[u].w, qok[u], v + 12);
+                }
+              }
+            } else if constexpr (MASKED) {
               widen32m(qx[u].x, qv[u].x, v + 0);
               if (!short_k) {
                 widen32m(qx[u].y, qv[u].y, v + 8);
@@ -897,7 +1088,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     const bool static_thr = ncols <= THR_COLS;
     if constexpr (EM == E_PACK || EM == E_POOLPACK) {
       if (static_thr) {
-        stage_thresholds(g, 0, ncols, et, 32 * NEPI, lane, sthr, sgm);
+        stage_thresholds<F4>(g, 0, ncols, et, 32 * NEPI, lane, sthr, sgm);
         epi_bar<NEPI>();
       }
     }
@@ -908,7 +1099,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       // [source rank][row][RS], then each owner sums its rows and packs them.
       static_assert(EM == E_PACK || EM == E_POOLPACK, "split-K kernels pack their output");
       constexpr int RS = BN + 4;  // padded slot row (ints): conflict-free 16-byte reads across rows
-      static_assert(BM * RS * 4 <= b_stages<BN, BKS>() * B_STAGE_BYTES, "reduction slots fit the B ring");
+      static_assert(BM * RS * 4 <= B_REGION, "reduction slots fit the B ring");
       const int64_t t = blockIdx.x;  // one item per CTA
       const int64_t tt = t / ksp;
       const int rank = (int)(t % ksp);
@@ -946,10 +1137,17 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int4 x = p[i];
-            v[4 * i] += x.x, v[4 * i + 1] += x.y, v[4 * i + 2] += x.z, v[4 * i + 3] += x.w;
+            if constexpr (F4) {  // exact: integer-valued floats below 2^24
+              v[4 * i] = __float_as_uint(__uint_as_float(v[4 * i]) + __int_as_float(x.x));
+              v[4 * i + 1] = __float_as_uint(__uint_as_float(v[4 * i + 1]) + __int_as_float(x.y));
+              v[4 * i + 2] = __float_as_uint(__uint_as_float(v[4 * i + 2]) + __int_as_float(x.z));
+              v[4 * i + 3] = __float_as_uint(__uint_as_float(v[4 * i + 3]) + __int_as_float(x.w));
+            } else {
+              v[4 * i] += x.x, v[4 * i + 1] += x.y, v[4 * i + 2] += x.z, v[4 * i + 3] += x.w;
+            }
           }
         }
-        uint32_t w = thr_word(v, sthr + ((n0 + chunk * 32) >> 1));
+        uint32_t w = thr_word<F4>(v, sthr + ((n0 + chunk * 32) >> 1));
         if constexpr (EM == E_POOLPACK) w = pool_word(w, sgm[(n0 >> 5) + chunk]);
         const int64_t m = mrow0 + row;
         const int wcol = n0 / 32 + chunk;
@@ -965,7 +1163,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       if constexpr (EM == E_PACK || EM == E_POOLPACK) {
         if (!static_thr) {  // N too wide for the resident table: this tile's columns only
           epi_bar<NEPI>();
-          stage_thresholds(g, n0, BN, et, 32 * NEPI, lane, sthr, sgm);
+          stage_thresholds<F4>(g, n0, BN, et, 32 * NEPI, lane, sthr, sgm);
           epi_bar<NEPI>();
         }
       }
@@ -997,7 +1195,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             for (int j = 0; j < 32; ++j) {
               const int n = nb + j;
               if (n < g.N)
-                o[j] = __dadd_rn(__dmul_rn(__dsub_rn((double)(int)v[j], __ldg(g.mean + n)), __ldg(g.scale + n)),
+                o[j] = __dadd_rn(__dmul_rn(__dsub_rn((double)acc_int<F4>(v[j]), __ldg(g.mean + n)), __ldg(g.scale + n)),
                                  __ldg(g.beta + n));
             }
           }
@@ -1007,15 +1205,16 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             if (nb + 32 <= g.N && ((g.ldo & 3) == 0)) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<int4*>(o + j) = make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+                *reinterpret_cast<int4*>(o + j) = make_int4(acc_int<F4>(v[j]), acc_int<F4>(v[j + 1]),
+                                                            acc_int<F4>(v[j + 2]), acc_int<F4>(v[j + 3]));
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (nb + j < g.N) o[j] = (int)v[j];
+                if (nb + j < g.N) o[j] = acc_int<F4>(v[j]);
             }
           }
         } else {
-          uint32_t w = thr_word(v, trow + c * 16);
+          uint32_t w = thr_word<F4>(v, trow + c * 16);
           if constexpr (EM == E_POOLPACK) w = pool_word(w, sgm[((tcol + ec0) >> 5) + c]);
           words[c] = w;
         }
@@ -1072,10 +1271,14 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   }
 }
 
-template <int BN, int AM, int BKS>
+template <int BN, int AM, int BKS, bool F4 = false>
 constexpr int smem_bytes() {
-  return b_stages<BN, BKS>() * BN * BKS + THR_COLS * 8 + THR_COLS / 8 +
-         8 * (2 * a_stages<BN, AM, BKS>() + 7) + 16 + 1024;
+  if constexpr (F4)
+    return f4_stages<BN, BKS>() * (BN + BM) * BKS / 2 + THR_COLS * 8 + THR_COLS / 8 +
+           8 * (2 * f4_stages<BN, BKS>() + 7) + 16 + 1024;
+  else
+    return b_stages<BN, BKS>() * BN * BKS + THR_COLS * 8 + THR_COLS / 8 + 8 * (2 * a_stages<BN, AM, BKS>() + 7) +
+           16 + 1024;
 }
 
 }  // namespace tc

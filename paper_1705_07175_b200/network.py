@@ -154,7 +154,8 @@ class _ByteConvFused(_Stage):
         self.tc = _lib.ENGINE == "tc" and rec.k <= 128 and c <= 8
         if not self.tc and (rec.k > 32 or rec.filters > 1024):
             raise AssertionError("planner chose the fused byte conv for an ineligible shape")
-        self.w8 = _dev.widen_i8(self.w, rec.filters, rec.k) if self.tc else None
+        self.fmt = _lib.TC_FORMAT
+        self.wt = _dev.tc_weights(self.w, rec.filters, rec.k, self.fmt) if self.tc else None
 
     def per_image(self):
         return (self.h_out * self.w_out, _wpl(self.rec.filters))
@@ -173,8 +174,8 @@ class _ByteConvFused(_Stage):
         h, w, c = self.in_shape
         r = self.rec
         if self.tc:
-            _lib.call("b2_tc_byte_conv_bn_pack", self.src_ptr(net), batch, h, w, c,
-                      _thresh_struct(self.bn0["thresh32"], self.bn0["thresh64"], self.bn0["ge"]), _dev.P(self.w8),
+            _lib.call(_lib.tc_entry("byte_conv_bn_pack", self.fmt), self.src_ptr(net), batch, h, w, c,
+                      _thresh_struct(self.bn0["thresh32"], self.bn0["thresh64"], self.bn0["ge"]), _dev.P(self.wt),
                       r.filters, r.kh, r.kw, r.stride, r.pad, 0,
                       _thresh_struct(self.bn1["thresh32"], self.bn1["thresh64"], self.bn1["ge"]), _dev.P(self.codes),
                       _dev.P(self.out), st)
@@ -197,7 +198,8 @@ class _ConvFused(_Stage):
         self.w = _dev.upload(rec.words)
         self.tc = _lib.ENGINE == "tc" and c % 64 == 0
         if self.tc:  # zero padding on the tensor cores: no correction map needed
-            self.w8, self.corr = _dev.widen_i8(self.w, rec.filters, rec.k), None
+            self.fmt = _lib.TC_FORMAT
+            self.wt, self.corr = _dev.tc_weights(self.w, rec.filters, rec.k, self.fmt), None
         else:
             self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
         if pool:
@@ -211,7 +213,7 @@ class _ConvFused(_Stage):
         h, w, c = self.in_shape
         r = self.rec
         if self.tc:
-            _lib.call("b2_tc_conv_bn_pack", self.src_ptr(net), batch, h, w, c, _dev.P(self.w8), r.filters, r.kh,
+            _lib.call(_lib.tc_entry("conv_bn_pack", self.fmt), self.src_ptr(net), batch, h, w, c, _dev.P(self.wt), r.filters, r.kh,
                       r.kw, r.stride, r.pad, int(self.pool),
                       _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]), _dev.P(self.out), st)
             return
@@ -233,7 +235,8 @@ class _Conv(_Stage):
         self.w = _dev.upload(rec.words)
         self.tc = _lib.ENGINE == "tc" and c % 64 == 0
         if self.tc:
-            self.w8, self.corr = _dev.widen_i8(self.w, rec.filters, rec.k), None
+            self.fmt = _lib.TC_FORMAT
+            self.wt, self.corr = _dev.tc_weights(self.w, rec.filters, rec.k, self.fmt), None
         else:
             self.corr = correction_device(self.w, rec.filters, in_shape, (rec.kh, rec.kw), rec.stride, rec.pad)
 
@@ -251,7 +254,7 @@ class _Conv(_Stage):
         h, w, c = self.in_shape
         r = self.rec
         if self.tc:
-            _lib.call("b2_tc_conv_forward", self.src_ptr(net), batch, h, w, c, _dev.P(self.w8), r.filters, r.kh,
+            _lib.call(_lib.tc_entry("conv_forward", self.fmt), self.src_ptr(net), batch, h, w, c, _dev.P(self.wt), r.filters, r.kh,
                       r.kw, r.stride, r.pad, _dev.P(self.out), st)
             return
         _lib.call("b2_conv_forward", self.src_ptr(net), batch, h, w, c, _dev.P(self.w), r.filters, r.kh, r.kw,
@@ -326,15 +329,16 @@ class _DenseFused(_Stage):
         super().__init__(src)
         self.rec, self.bn = rec, bn_dev
         self.w = _dev.upload(rec.words)
-        self.w8 = _dev.widen_i8(self.w, rec.units, rec.input_len) if _lib.ENGINE == "tc" else None
+        self.fmt = _lib.TC_FORMAT
+        self.wt = _dev.tc_weights(self.w, rec.units, rec.input_len, self.fmt) if _lib.ENGINE == "tc" else None
 
     def per_image(self):
         return (_wpl(self.rec.units),)
 
     def launch(self, net, batch, st):
         r = self.rec
-        if self.w8 is not None and batch >= max(TC_MIN_ROWS, TC_MIN_ROWS_DENSE):
-            _lib.call("b2_tc_dense_bn_pack", self.src_ptr(net), batch, _dev.P(self.w8), r.units, _wpl(r.input_len),
+        if self.wt is not None and batch >= max(TC_MIN_ROWS, TC_MIN_ROWS_DENSE):
+            _lib.call(_lib.tc_entry("dense_bn_pack", self.fmt), self.src_ptr(net), batch, _dev.P(self.wt), r.units, _wpl(r.input_len),
                       r.input_len, _thresh_struct(self.bn["thresh32"], self.bn["thresh64"], self.bn["ge"]),
                       _dev.P(self.out), st)
             return
@@ -351,15 +355,16 @@ class _Dense(_Stage):
         super().__init__(src)
         self.rec = rec
         self.w = _dev.upload(rec.words)
-        self.w8 = _dev.widen_i8(self.w, rec.units, rec.input_len) if _lib.ENGINE == "tc" else None
+        self.fmt = _lib.TC_FORMAT
+        self.wt = _dev.tc_weights(self.w, rec.units, rec.input_len, self.fmt) if _lib.ENGINE == "tc" else None
 
     def per_image(self):
         return (self.rec.units,)
 
     def launch(self, net, batch, st):
         r = self.rec
-        if self.w8 is not None and batch >= max(TC_MIN_ROWS, TC_MIN_ROWS_DENSE):
-            _lib.call("b2_tc_bgemm", self.src_ptr(net), batch, _dev.P(self.w8), r.units, _wpl(r.input_len),
+        if self.wt is not None and batch >= max(TC_MIN_ROWS, TC_MIN_ROWS_DENSE):
+            _lib.call(_lib.tc_entry("bgemm", self.fmt), self.src_ptr(net), batch, _dev.P(self.wt), r.units, _wpl(r.input_len),
                       r.input_len, _dev.P(self.out), st)
             return
         _lib.call("b2_bgemv", _dev.P(self.w), r.units, _wpl(r.input_len), self.src_ptr(net), batch, r.input_len,
@@ -396,7 +401,7 @@ class _DenseFinal(_Stage):
             self.dense.launch(net, batch, st)
             self.final.launch(net, batch, st)
             return
-        _lib.call("b2_tc_dense_affine_f64", self.src_ptr(net), batch, _dev.P(self.dense.w8), r.units,
+        _lib.call(_lib.tc_entry("dense_affine_f64", self.dense.fmt), self.src_ptr(net), batch, _dev.P(self.dense.wt), r.units,
                   _wpl(r.input_len), r.input_len, _dev.P(self.bn["mean64"]), _dev.P(self.bn["scale64"]),
                   _dev.P(self.bn["beta64"]), self.out_ptr(net), st)
 

@@ -68,11 +68,12 @@ def random_mlp(rng):
     return ModelSpec((1, 1, k), recs)
 
 
-@pytest.mark.parametrize("engine", ["tc", "popc"])
+@pytest.mark.parametrize("engine", ["tc", "tc8", "popc"])  # tc: fp4 tensor-core operands, tc8: int8
 @pytest.mark.parametrize("seed", range(16))
 def test_random_networks_vs_oracle(oracle, seed, engine, monkeypatch):
     from paper_1705_07175_b200 import _lib
-    monkeypatch.setattr(_lib, "ENGINE", engine)
+    monkeypatch.setattr(_lib, "ENGINE", "tc" if engine == "tc8" else engine)
+    monkeypatch.setattr(_lib, "TC_FORMAT", "i8" if engine == "tc8" else "f4")
     rng = np.random.default_rng(9000 + seed)
     spec = random_cnn(rng) if seed % 3 else random_mlp(rng)
     h, w, c = spec.input_dims

@@ -14,6 +14,12 @@ from paper_1705_07175_b200.network import Network
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["f4", "i8"])
+def fmt(request):
+    """Tensor-core weight format: kind::mxf4 e2m1 or kind::i8."""
+    return request.param
+
+
 def rand_pm1(rng, *shape):
     return np.where(rng.random(shape) < 0.5, -1.0, 1.0).astype(np.float32)
 
@@ -30,21 +36,21 @@ def th(cal):
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (5, 3, 63), (128, 128, 128), (129, 127, 129), (300, 200, 300),
                                    (64, 257, 1000), (1000, 333, 4096), (257, 1024, 1152), (100, 64, 16384),
                                    (513, 300, 2304)])
-def test_tc_bgemm_vs_oracle(oracle, m, n, k):
+def test_tc_bgemm_vs_oracle(oracle, m, n, k, fmt):
     rng = np.random.default_rng(m * 7 + n * 13 + k)
     a = oracle.pack_lines(rand_pm1(rng, m, k))
     b = oracle.pack_lines(rand_pm1(rng, n, k))
-    got = gemm.bgemm_device(_dev.upload(a), m, _dev.upload(b), n, a.shape[1], k, engine="tc")
+    got = gemm.bgemm_device(_dev.upload(a), m, _dev.upload(b), n, a.shape[1], k, engine="tc", fmt=fmt)
     assert np.array_equal(_dev.download(got, np.int32), oracle.bgemm(a, b, k))
 
 
-def test_tc_and_popc_engines_agree():
+def test_tc_and_popc_engines_agree(fmt):
     rng = np.random.default_rng(11)
     for m, n, k in ((2048, 512, 4608), (777, 129, 65)):
         a = _dev.upload(zoo.pack_bits_host(rng.random((m, k)) >= 0.5))
         b = _dev.upload(zoo.pack_bits_host(rng.random((n, k)) >= 0.5))
         wpl = -(-k // 64)
-        tc = _dev.download(gemm.bgemm_device(a, m, b, n, wpl, k, engine="tc"), np.int32)
+        tc = _dev.download(gemm.bgemm_device(a, m, b, n, wpl, k, engine="tc", fmt=fmt), np.int32)
         pc = _dev.download(gemm.bgemm_device(a, m, b, n, wpl, k, engine="popc"), np.int32)
         assert np.array_equal(tc, pc), (m, n, k)
 
@@ -56,7 +62,7 @@ CONV_CASES = [  # h, w, c, f, kh, kw, stride, pad, batch
 
 
 @pytest.mark.parametrize("h,w,c,f,kh,kw,stride,pad,batch", CONV_CASES)
-def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batch):
+def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batch, fmt):
     rng = np.random.default_rng(h * 31 + c + f)
     xs = np.stack([oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)])
     wt = oracle.pack_lines(rand_pm1(rng, f, kh * kw * c))
@@ -65,9 +71,9 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
     want = np.stack([oracle.bgemm(oracle.unroll_packed(x, h, w, c, kh, kw, stride, pad), wt, kh * kw * c) + corr
                      for x in xs]).reshape(batch, ho, wo, f)
     wd = _dev.upload(wt)
-    w8 = _dev.widen_i8(wd, f, kh * kw * c)
+    w8 = _dev.tc_weights(wd, f, kh * kw * c, fmt)
     out = _dev.empty((batch, ho, wo, f), np.int32)
-    _lib.call("b2_tc_conv_forward", _dev.P(_dev.upload(xs)), batch, h, w, c, _dev.P(w8), f, kh, kw, stride, pad,
+    _lib.call(_lib.tc_entry("conv_forward", fmt), _dev.P(_dev.upload(xs)), batch, h, w, c, _dev.P(w8), f, kh, kw, stride, pad,
               _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.int32), want)
 
@@ -81,7 +87,7 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
                                                 (4, 4, 512, 512, True, 1), (8, 8, 512, 200, False, 3),
                                                 (6, 6, 512, 130, True, 2), (8, 8, 1024, 64, False, 1),
                                                 (2, 2, 512, 2048, True, 1)])
-def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch):
+def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch, fmt):
     rng = np.random.default_rng(5 + h + c + f)
     xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
     wt = oracle.pack_lines(rand_pm1(rng, f, 9 * c))
@@ -98,10 +104,10 @@ def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch):
         want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn.thresh, bn.ge_dir, False))
     cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 9 * c)
     wd = _dev.upload(wt)
-    w8 = _dev.widen_i8(wd, f, 9 * c)
+    w8 = _dev.tc_weights(wd, f, 9 * c, fmt)
     sites = h * w // (4 if pool else 1)
     out = _dev.empty((batch, sites, -(-f // 64)), np.uint64)
-    _lib.call("b2_tc_conv_bn_pack", _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1,
+    _lib.call(_lib.tc_entry("conv_bn_pack", fmt), _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1,
               int(pool), th(cal), _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
 
@@ -111,7 +117,7 @@ def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch):
 @pytest.mark.parametrize("batch,units,k", [(1, 300, 4096), (5, 64, 1000), (37, 1024, 8192), (200, 4096, 4096),
                                            (129, 10, 1024), (300, 130, 300), (64, 1000, 784),
                                            (17, 64, 3600), (130, 200, 4096), (5, 2048, 16384), (3, 100, 5000)])
-def test_tc_dense_bn_pack_vs_oracle(oracle, batch, units, k):
+def test_tc_dense_bn_pack_vs_oracle(oracle, batch, units, k, fmt):
     rng = np.random.default_rng(batch + units + k)
     x = oracle.pack_lines(rand_pm1(rng, batch, k))
     wt = oracle.pack_lines(rand_pm1(rng, units, k))
@@ -120,9 +126,9 @@ def test_tc_dense_bn_pack_vs_oracle(oracle, batch, units, k):
     want = np.stack([oracle.threshold_sign_pack(acc[i].reshape(1, -1), bn.thresh, bn.ge_dir, True)[0]
                      for i in range(batch)])
     cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, k)
-    w8 = _dev.widen_i8(_dev.upload(wt), units, k)
+    w8 = _dev.tc_weights(_dev.upload(wt), units, k, fmt)
     out = _dev.empty((batch, -(-units // 64)), np.uint64)
-    _lib.call("b2_tc_dense_bn_pack", _dev.P(_dev.upload(x)), batch, _dev.P(w8), units, -(-k // 64), k, th(cal),
+    _lib.call(_lib.tc_entry("dense_bn_pack", fmt), _dev.P(_dev.upload(x)), batch, _dev.P(w8), units, -(-k // 64), k, th(cal),
               _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.uint64), want)
 
@@ -149,7 +155,7 @@ def test_tc_input8_bn_pack_vs_oracle(oracle, batch, units, k):
 @pytest.mark.parametrize("h,w,c,f,kh,pad,stride,pool", [(32, 32, 3, 128, 3, 1, 1, False), (16, 12, 3, 64, 3, 1, 1, True),
                                                         (9, 9, 4, 200, 5, 2, 2, False), (8, 8, 8, 32, 3, 1, 1, True), (10, 6, 5, 64, 5, 2, 1, True),
                                                         (5, 7, 1, 10, 3, 0, 1, False)])
-def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, pool):
+def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, pool, fmt):
     rng = np.random.default_rng(h * w + c + f)
     batch = 3
     imgs = rng.integers(0, 256, (batch, h, w, c), dtype=np.uint8)
@@ -174,11 +180,11 @@ def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, poo
         want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn1.thresh, bn1.ge_dir, False))
     cal0 = layers.calibrate_device(bn0.mean, bn0.var, bn0.gamma, bn0.beta, bn0.eps, 255)
     cal1 = layers.calibrate_device(bn1.mean, bn1.var, bn1.gamma, bn1.beta, bn1.eps, k)
-    w8 = _dev.widen_i8(_dev.upload(wt), f, k)
+    w8 = _dev.tc_weights(_dev.upload(wt), f, k, fmt)
     sites = ho * wo // (4 if pool else 1)
     out = _dev.empty((batch, sites, -(-f // 64)), np.uint64)
     codes = _dev.empty((_lib.raw("b2_tc_byte_conv_scratch_bytes")(batch, h, w, c, kh, kh, stride, pad),), np.uint8)
-    _lib.call("b2_tc_byte_conv_bn_pack", _dev.P(_dev.upload(imgs)), batch, h, w, c, th(cal0), _dev.P(w8), f, kh, kh,
+    _lib.call(_lib.tc_entry("byte_conv_bn_pack", fmt), _dev.P(_dev.upload(imgs)), batch, h, w, c, th(cal0), _dev.P(w8), f, kh, kh,
               stride, pad, int(pool), th(cal1), _dev.P(codes), _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
 
@@ -298,7 +304,7 @@ def test_bcnn_batch_65536(networks_golden):
 
 @pytest.mark.parametrize("batch", [1, 3, 100])
 @pytest.mark.parametrize("units,k", [(10, 64), (200, 4608), (32, 32), (65, 100), (130, 1000)])
-def test_packed_outputs_fully_written(oracle, batch, units, k):
+def test_packed_outputs_fully_written(oracle, batch, units, k, fmt):
     """Every kernel writes its whole `out` (include/bitnn_b200.h): packed
     lines are padded to whole uint64 words and the padding bits must come out
     0 even when the buffer held garbage (the next layer XORs them)."""
@@ -311,16 +317,16 @@ def test_packed_outputs_fully_written(oracle, batch, units, k):
         np.stack([oracle.threshold_sign_pack(r.reshape(1, -1), bn.thresh, bn.ge_dir, True)[0]
                   for r in oracle.bgemm(x, wt, k)])
     want = want.reshape(batch, -1)
-    for name in ("b2_dense_bn_pack", "b2_tc_dense_bn_pack"):
+    for name in ("b2_dense_bn_pack", _lib.tc_entry("dense_bn_pack", fmt)):
         out = _dev.upload(np.full((batch, -(-units // 64)), 0xFFFFFFFFFFFFFFFF, np.uint64))
-        wd = _dev.upload(wt) if name == "b2_dense_bn_pack" else _dev.widen_i8(_dev.upload(wt), units, k)
+        wd = _dev.upload(wt) if name == "b2_dense_bn_pack" else _dev.tc_weights(_dev.upload(wt), units, k, fmt)
         _lib.call(name, _dev.P(_dev.upload(x)), batch, _dev.P(wd), units, -(-k // 64), k, th(cal), _dev.P(out),
                   _dev.stream())
         assert np.array_equal(_dev.download(out, np.uint64), want), name
 
 
 @pytest.mark.parametrize("seed", range(30))
-def test_tc_conv_forward_random_geometry(oracle, seed):
+def test_tc_conv_forward_random_geometry(oracle, seed, fmt):
     rng = np.random.default_rng(4000 + seed)
     c = int(rng.choice([64, 128, 192, 256, 320]))
     kh, kw = int(rng.integers(1, 6)), int(rng.integers(1, 6))
@@ -334,15 +340,15 @@ def test_tc_conv_forward_random_geometry(oracle, seed):
     ho, wo = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
     want = np.stack([oracle.bgemm(oracle.unroll_packed(x, h, w, c, kh, kw, stride, pad), wt, kh * kw * c) + corr
                      for x in xs]).reshape(batch, ho, wo, f)
-    w8 = _dev.widen_i8(_dev.upload(wt), f, kh * kw * c)
+    w8 = _dev.tc_weights(_dev.upload(wt), f, kh * kw * c, fmt)
     out = _dev.upload(np.full((batch, ho, wo, f), -7, np.int32))
-    _lib.call("b2_tc_conv_forward", _dev.P(_dev.upload(xs)), batch, h, w, c, _dev.P(w8), f, kh, kw, stride, pad,
+    _lib.call(_lib.tc_entry("conv_forward", fmt), _dev.P(_dev.upload(xs)), batch, h, w, c, _dev.P(w8), f, kh, kw, stride, pad,
               _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.int32), want), (h, w, c, f, kh, kw, stride, pad, batch)
 
 
 @pytest.mark.parametrize("seed", range(20))
-def test_tc_conv_bn_pack_random_geometry(oracle, seed):
+def test_tc_conv_bn_pack_random_geometry(oracle, seed, fmt):
     rng = np.random.default_rng(5000 + seed)
     c = int(rng.choice([64, 128, 256]))
     pool = bool(rng.integers(0, 2))
@@ -359,9 +365,9 @@ def test_tc_conv_bn_pack_random_geometry(oracle, seed):
             acc = oracle.maxpool(acc, 2, 2, 2)
         want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn.thresh, bn.ge_dir, False))
     cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 9 * c)
-    w8 = _dev.widen_i8(_dev.upload(wt), f, 9 * c)
+    w8 = _dev.tc_weights(_dev.upload(wt), f, 9 * c, fmt)
     sites = h * w // (4 if pool else 1)
     out = _dev.upload(np.full((batch, sites, -(-f // 64)), 0xFFFFFFFFFFFFFFFF, np.uint64))
-    _lib.call("b2_tc_conv_bn_pack", _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1,
+    _lib.call(_lib.tc_entry("conv_bn_pack", fmt), _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1,
               int(pool), th(cal), _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.uint64), np.stack(want)), (h, w, c, f, pool, batch)
