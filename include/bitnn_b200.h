@@ -244,6 +244,39 @@ int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c
                             const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
                             b2_thresh th_out, void* scratch, uint64_t* out, void* stream);
 
+/* ---------------------------------------------------------------- fp4 tensor-core path
+ *
+ * The same operators on tcgen05.mma kind::mxf4: +1 / -1 / 0 are exact e2m1
+ * values (0x2 / 0xA / 0x0), the block scales are all 2^0, and the fp32
+ * accumulator holds the exact integer dot product (|dot| < 2^24).  Twice the
+ * int8 MMA rate and half the operand bytes.  Weights come from
+ * b2_expand_f4; each b2_tc4_X takes exactly the arguments of b2_tc_X with
+ * its weight pointer in that format.  Results are identical to b2_tc_X. */
+
+/* K rounded up to the 1024-element granule of the fp4 weight rows. */
+int64_t b2_f4_kpad(int64_t k);
+
+/* Packed +/-1 lines -> e2m1 nibbles for the fp4 path: w (rows, wpl) with k
+ * valid bits -> out (rows, b2_f4_kpad(k) / 2) bytes; K permuted inside each
+ * 32-group like the on-chip widening of the A operand; 0 beyond k. */
+int b2_expand_f4(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, uint8_t* out, void* stream);
+
+int b2_tc4_bgemm(const uint64_t* a, int64_t m, const int8_t* b_f4, int64_t n, int64_t wpl, int32_t k, int32_t* out,
+                 void* stream);
+int b2_tc4_dense_affine_f64(const uint64_t* x, int64_t batch, const int8_t* w_f4, int64_t units, int64_t wpl,
+                            int32_t k, const double* mean, const double* scale, const double* beta, double* out,
+                            void* stream);
+int b2_tc4_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_f4, int64_t units, int64_t wpl, int32_t k,
+                         b2_thresh th, uint64_t* out, void* stream);
+int b2_tc4_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_f4,
+                        int64_t filters, int kh, int kw, int stride, int pad, int32_t* out, void* stream);
+int b2_tc4_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_f4,
+                        int64_t filters, int kh, int kw, int stride, int pad, int pool, b2_thresh th, uint64_t* out,
+                        void* stream);
+int b2_tc4_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
+                             const int8_t* w_f4, int64_t filters, int kh, int kw, int stride, int pad, int pool,
+                             b2_thresh th_out, void* scratch, uint64_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
