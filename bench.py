@@ -167,6 +167,47 @@ def measure_int8_peak(dev, n: int = 8192, reps: int = 10):
                                            f"torch._int_mm unavailable: {exc}"
 
 
+def measure_fp4_peak(dev, n: int = 8192, reps: int = 10):
+    """Dense fp4 tensor-core peak of THIS GPU, measured: cuBLASLt block-scaled
+    fp4 GEMM (torch._scaled_mm on float4_e2m1fn_x2 with block-16 e4m3 scales,
+    NVFP4 — the same tensor rate as the MXFP4 kind::mxf4 MMAs this framework
+    issues) on n^3, best of `reps`, CUDA events.  One binary MAC is one fp4
+    MAC on +/-1 values (2 ops)."""
+    import torch
+    try:
+        a = torch.randint(0, 256, (n, n // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
+        b = torch.randint(0, 256, (n, n // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
+        sa = torch.full((n * (n // 16),), 0x38, dtype=torch.uint8, device=dev).view(torch.float8_e4m3fn)
+        sb = torch.full((n * (n // 16),), 0x38, dtype=torch.uint8, device=dev).view(torch.float8_e4m3fn)
+        f = lambda: torch._scaled_mm(a, b.t(), sa, sb, out_dtype=torch.bfloat16)  # noqa: E731
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            f()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b, sa, sb
+        return 2.0 * n ** 3 / (best / 1e3) / 1e12, (f"cuBLASLt NVFP4 GEMM (torch._scaled_mm, e2m1 x e2m1, block-16 "
+                                                    f"e4m3 scales) {n}^3, best of {reps}, this GPU")
+    except Exception as exc:  # pragma: no cover - library without fp4 GEMM
+        return 9000.0, f"B200_PROFILING.md dense fp4 9 PFLOP/s (fallback: torch fp4 GEMM unavailable: {exc})"
+
+
+def stage_format(st) -> str:
+    """Operand format of a stage's GEMM: "f4" / "i8" tensor cores or "popc"."""
+    from paper_1705_07175_b200 import _lib
+    if _lib.ENGINE != "tc" or not (getattr(st, "tc", True)):
+        return "popc"
+    if getattr(st, "name", "").startswith("input8"):
+        return "i8"
+    return getattr(st, "fmt", None) or getattr(getattr(st, "dense", None), "fmt", None) or "i8"
+
+
 # --------------------------------------------------------------------------- workloads
 
 def build_workload(name):
@@ -312,21 +353,26 @@ def run_ours(args, rank, world, local_rank):
             st.launch(net, B, _dev_stream())
         b.record(stream)
         torch.cuda.synchronize()
-        stages.append({"stage": st.name, "ms": a.elapsed_time(b) / reps, "bitops": 2 * stage_macs(st) * B})
+        stages.append({"stage": st.name, "ms": a.elapsed_time(b) / reps, "bitops": 2 * stage_macs(st) * B,
+                       "format": stage_format(st)})
     stage_total = sum(s["ms"] for s in stages)
     batch1 = batch1_latency(spec, shape) if rank == 0 else None
     others = other_metrics(args, dev, flush) if rank == 0 and not args.no_extra else None
     int8_peak, int8_src = measure_int8_peak(dev)
+    fp4_peak, fp4_src = measure_fp4_peak(dev)
+    peaks = {"f4": (fp4_peak, fp4_src), "i8": (int8_peak, int8_src), "popc": (POPC_PEAK_TBITOPS, POPC_PEAK_SOURCE)}
     for s_ in stages:
         s_["tops"] = s_["bitops"] / (s_["ms"] / 1e3) / 1e12 if s_["ms"] > 0 else 0.0
-        s_["frac_of_int8_peak"] = s_["tops"] / int8_peak
+        s_["frac_of_peak"] = s_["tops"] / peaks[s_["format"]][0]
     dom = max(stages, key=lambda s_: s_["ms"])
     achieved = dom["tops"]
+    dom_peak, dom_src = peaks[dom["format"]]
     traffic = stage_traffic(args.workload, dom["stage"], stages.index(dom))
     result = {
         "metric": BASELINE_METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u1 packed (+/-1) activations, s8 tensor-core operands, s32 acc, f64 scores",
+        "vs_baseline": None, "dtype": "u1 packed (+/-1) activations; tensor-core operands e2m1 (fp4, unit block scales) "
+                 "or s8 (u8-input layer), exact fp32 / s32 accumulators; f64 scores",
         "data": "synthetic",
         "config": config_dict(args) | {"global_batch": B * world, "engine": _lib.ENGINE},
         "clocks": clk.summary(),
@@ -335,10 +381,11 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(gpu_launches),
         "bitops_per_image": 2 * zoo.macs_per_image(spec),
         "achieved_tbitops_network": 2 * zoo.macs_per_image(spec) * value / world / 1e12,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
-                     "unit": "TOP/s (1 binary MAC = 2 ops = one int8 MAC on +/-1 bytes)",
-                     "frac": achieved / int8_peak, "traffic": traffic, "kernel": dom["stage"],
-                     "kernel_share_of_step": dom["ms"] / stage_total, "peak_source": int8_src,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": dom_peak,
+                     "unit": "TOP/s (1 binary MAC = 2 ops = one fp4 / int8 MAC on +/-1 operands)",
+                     "frac": achieved / dom_peak, "traffic": traffic, "kernel": dom["stage"],
+                     "operand_format": dom["format"], "kernel_share_of_step": dom["ms"] / stage_total,
+                     "peak_source": dom_src, "fp4_peak": fp4_peak, "int8_peak": int8_peak, "int8_peak_source": int8_src,
                      "popc_pipe_peak": POPC_PEAK_TBITOPS, "popc_peak_source": POPC_PEAK_SOURCE},
         "stages": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in s_.items()} for s_ in stages],
         "batch1": batch1,
@@ -352,7 +399,7 @@ def other_metrics(args, dev, flush, steps: int = 10):
     `value`: the other network (BMLP for a BCNN run and vice versa) and the
     bit-packed GEMM at M=N=K=8192 (configs[2])."""
     import torch
-    from paper_1705_07175_b200 import _dev, gemm, zoo
+    from paper_1705_07175_b200 import _dev, _lib, gemm, zoo
     from paper_1705_07175_b200.network import Network
     out = {}
     other = "bmlp" if args.workload == "bcnn" else "bcnn"
@@ -379,7 +426,7 @@ def other_metrics(args, dev, flush, steps: int = 10):
     rng = np.random.default_rng(6)
     a = _dev.upload(zoo.pack_bits_host(rng.random((n, n)) >= 0.5))
     w = _dev.upload(zoo.pack_bits_host(rng.random((n, n)) >= 0.5))
-    w8 = _dev.widen_i8(w, n, n)
+    w8 = _dev.tc_weights(w, n, n)  # tensor-core weights in the default operand format
     c = _dev.empty((n, n), np.int32)
     for _ in range(3):
         gemm.bgemm_device(a, n, w, n, n // 64, n, c, b_i8=w8)
@@ -393,6 +440,7 @@ def other_metrics(args, dev, flush, steps: int = 10):
         torch.cuda.synchronize()
         ms += e0.elapsed_time(e1)
     out["bgemm_8192_Gops"] = 2.0 * n ** 3 * 5 / (ms / 1e3) / 1e9
+    out["bgemm_operand_format"] = _lib.TC_FORMAT
     out["note"] = "device time, CUDA events, L2 flushed between steps; ops = 2 per binary MAC"
     return out
 

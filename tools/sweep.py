@@ -54,8 +54,9 @@ def bgemm_case(n, engine, flush, reps):
     a = _dev.upload(zoo.pack_bits_host(rng.random((n, n)) >= 0.5))
     b = _dev.upload(zoo.pack_bits_host(rng.random((n, n)) >= 0.5))
     out = _dev.empty((n, n), np.int32)
-    b8 = _dev.widen_i8(b, n, n) if engine == "tc" else None
-    ms = timed(lambda: gemm.bgemm_device(a, n, b, n, wpl, n, out, engine=engine, b_i8=b8), reps, flush)
+    fmt = _lib.TC_FORMAT
+    b8 = _dev.tc_weights(b, n, n, fmt) if engine == "tc" else None
+    ms = timed(lambda: gemm.bgemm_device(a, n, b, n, wpl, n, out, engine=engine, b_i8=b8, fmt=fmt), reps, flush)
     # spot-check 64 entries against the packed definition on the host
     ah, bh = _dev.download(a, np.uint64), _dev.download(b, np.uint64)
     got = _dev.download(out, np.int32)
@@ -63,7 +64,7 @@ def bgemm_case(n, engine, flush, reps):
         ref = n - 2 * int(np.bitwise_count(ah[i] ^ bh[j]).sum())
         assert got[i, j] == ref, (n, i, j)
     ops = 2.0 * n ** 3
-    return {"case": "bgemm", "engine": engine, "M": n, "N": n, "K": n, "ms": round(ms, 4),
+    return {"case": "bgemm", "engine": engine if engine != "tc" else "tc-" + fmt, "M": n, "N": n, "K": n, "ms": round(ms, 4),
             "Tops": round(ops / (ms / 1e3) / 1e12, 1), "Gops": round(ops / (ms / 1e3) / 1e9)}
 
 
@@ -71,20 +72,20 @@ def conv_case(c, hw, batch, flush, reps):
     rng = np.random.default_rng(c * 100 + hw)
     x = _dev.upload(zoo.pack_bits_host(rng.random((batch * hw * hw, c)) >= 0.5))
     w = _dev.upload(zoo.pack_bits_host(rng.random((c, 9 * c)) >= 0.5))
-    w8 = _dev.widen_i8(w, c, 9 * c)
+    w8 = _dev.tc_weights(w, c, 9 * c)
     bn = zoo.rand_bn(rng, c, 20.0)
     cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 9 * c)
     th = layers._thresh_struct(cal["thresh32"], cal["thresh64"], cal["ge"])
     out = _dev.empty((batch, hw * hw, -(-c // 64)), np.uint64)
 
     def run():
-        _lib.call("b2_tc_conv_bn_pack", _dev.P(x), batch, hw, hw, c, _dev.P(w8), c, 3, 3, 1, 1, 0,
+        _lib.call(_lib.tc_entry("conv_bn_pack"), _dev.P(x), batch, hw, hw, c, _dev.P(w8), c, 3, 3, 1, 1, 0,
                   layers._thresh_struct(cal["thresh32"], cal["thresh64"], cal["ge"]), _dev.P(out), _dev.stream())
 
     del th
     ms = timed(run, reps, flush)
     ops = 2.0 * batch * hw * hw * c * 9 * c
-    return {"case": "conv3x3", "engine": "tc", "C": c, "HW": hw, "batch": batch, "ms": round(ms, 4),
+    return {"case": "conv3x3", "engine": "tc-" + _lib.TC_FORMAT, "C": c, "HW": hw, "batch": batch, "ms": round(ms, 4),
             "Tops": round(ops / (ms / 1e3) / 1e12, 1), "images_per_s": round(batch / (ms / 1e3))}
 
 
