@@ -154,7 +154,9 @@ class _ByteConvFused(_Stage):
         self.tc = _lib.ENGINE == "tc" and rec.k <= 128 and c <= 8
         if not self.tc and (rec.k > 32 or rec.filters > 1024):
             raise AssertionError("planner chose the fused byte conv for an ineligible shape")
-        self.fmt = _lib.TC_FORMAT
+        # one K=32/64 MMA per tile: the kernel is producer/epilogue-bound and
+        # the int8 form (TMEM operand, 8-column stores) measured faster than fp4
+        self.fmt = "i8"
         self.wt = _dev.tc_weights(self.w, rec.filters, rec.k, self.fmt) if self.tc else None
 
     def per_image(self):
