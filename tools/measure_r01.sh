@@ -1,4 +1,5 @@
 # Round-1 measurement set (run on the GPU box from the repo root); outputs in gpurun_out/m_*
+# (fp4 tensor-core path default; the i8 path is benched alongside with B2_TC_FORMAT=i8)
 set -x
 timeout 300 python -m pytest tests -q -m gpu --timeout 300 > gpurun_out/m_pytest.txt 2>&1
 python bench.py > gpurun_out/m_bench_bcnn.json 2> gpurun_out/m_bench_bcnn.err
@@ -14,4 +15,10 @@ done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm -s 9 -c 1 -o gpurun_out/m_conv2_full python tools/profile_stage.py --stage 1 --reps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm -s 10 -c 1 -o gpurun_out/m_conv4_full python tools/profile_stage.py --stage 3 --reps 1 > /dev/null 2>&1
 timeout 900 python tools/sweep.py > gpurun_out/m_sweeps.jsonl 2> gpurun_out/m_sweeps.err
+(cd tools/microbench && nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o mxf4_rate mxf4_rate.cu) && timeout 120 ./tools/microbench/mxf4_rate > gpurun_out/m_mxf4_rate.jsonl 2>&1
+python tools/_fp4_peak.py > gpurun_out/m_lib_peaks.txt 2>&1
+python tools/_b1_breakdown.py > gpurun_out/m_batch1.txt 2>&1
+python tools/_pipe_probe.py > gpurun_out/m_pipe.txt 2>&1
+B2_TC_FORMAT=i8 python bench.py --steps 20 --warmup 5 --no-extra --no-cpu > gpurun_out/m_bench_bcnn_i8.json 2>&1
+B2_TC_FORMAT=i8 python bench.py --workload bmlp --steps 20 --warmup 5 --no-extra --no-cpu > gpurun_out/m_bench_bmlp_i8.json 2>&1
 ls gpurun_out
