@@ -8,6 +8,7 @@
 #include <stdlib.h>
 
 #include "tc_i8.cuh"
+#include "tc_padrow.cuh"
 
 #ifndef B2_RESIDENT_B
 #define B2_RESIDENT_B 1
@@ -394,6 +395,90 @@ inline void conv_args(Args& g, const void* x, int64_t batch, int h, int w, int c
   g.kw_magic = ((1ull << 32) + (uint64_t)kw - 1) / (uint64_t)kw;
 }
 
+// Padded-row implicit GEMM (tc_padrow.cuh) for the fp4 conv: stride 1,
+// same-size output, odd kh == kw with pad = (k - 1) / 2, c % 128 == 0,
+// at most 128 filters, weights resident (K <= 1536).
+#ifndef B2_PADROW
+#define B2_PADROW 1
+#endif
+inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t batch) {
+  static const int on = [] {
+    const char* e = getenv("B2_PADROW");
+    return e ? atoi(e) : B2_PADROW;
+  }();
+  return on && g.stride == 1 && g.Ho == g.H && g.Wo == g.W && g.kh == g.kw && (g.kh & 1) && g.pad == (g.kh - 1) / 2 &&
+         c % 128 == 0 && filters <= 128 && k <= 1536 && g.W < 4096 && wpl64(filters) <= 32 &&
+         (int64_t)g.kh * g.kw * (c / 64) <= 128 &&
+         // enough tiles to fill the GPU (small batches keep the one-launch path)
+         (int64_t)(g.H + 1) * (g.W + 1) * batch >= (int64_t)BM * num_sms();
+}
+
+inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c, const int8_t* w_f4, int64_t filters,
+                         int64_t k, int pool, uint64_t* out, cudaStream_t st) {
+  PadArgs p{};
+  p.x = reinterpret_cast<const uint32_t*>(lines);
+  p.N = (int)batch;
+  p.H = g.H;
+  p.W = g.W;
+  p.sstride = g.sstride;
+  p.P = c / 32;
+  p.kh = g.kh;
+  p.kw = g.kw;
+  p.pad = g.pad;
+  p.Wp = g.W + 1;
+  p.VI = (int64_t)(g.H + 1) * p.Wp;
+  p.Vtotal = p.VI * batch;
+  p.R8 = ((2 * p.Wp + 2 + BM) + 7) / 8 * 8;
+  p.nkb = (int)((k + 255) / 256);
+  p.F = (int)filters;
+  p.kmmas = p.P / 2;
+  p.ldo32 = 2 * wpl64(filters);
+  p.thresh = g.thresh;
+  p.ge = g.ge;
+  // band rows x planes must fit a slot, and the producers' 2 x 256 units cover it
+  if ((int64_t)p.R8 * 16 * p.P > PR_BAND_MAX || (int64_t)p.R8 * (p.P / 4) > 2 * 32 * PR_NPW || batch > INT32_MAX)
+    return B2_EINVAL;
+  CUtensorMap map;
+  if (int rc = make_bmap(&map, w_f4, filters, kpad_f4(k) / 2, 128)) return rc;
+  const int smem = padrow_smem_bytes(p.nkb);
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(k_padrow_conv, smem, attr);
+  const int64_t tiles = (p.Vtotal + BM - 1) / BM;
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  void* scratch = nullptr;
+  if (pool) {  // unpooled thresholded bits, then the 2x2 OR/AND combine
+    // stream-ordered scratch (capturable into graphs); keep the device's
+    // default pool from returning it to the OS between calls
+    static std::atomic<uint64_t> pool_kept{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(pool_kept.load() & (1ull << (dev & 63)))) {
+      cudaMemPool_t mp;
+      if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pool_kept.fetch_or(1ull << (dev & 63));
+    }
+    if (cudaMallocAsync(&scratch, (size_t)batch * g.H * g.W * p.ldo32 * 4, st) != cudaSuccess) return launched();
+    p.out_bits = reinterpret_cast<uint32_t*>(scratch);
+  } else {
+    p.out_bits = reinterpret_cast<uint32_t*>(out);
+  }
+  launch_k(k_padrow_conv, grid, 32 * (4 + PR_NPW + PR_NEPI), smem, st, map, p);
+  int rc = launched();
+  if (pool) {
+    if (!rc) {
+      const int64_t n = batch * (g.H / 2) * (g.W / 2) * p.ldo32;
+      launch_k(k_pool_bits, (unsigned)cdiv(n, 256), 256, 0, st, (const uint32_t*)scratch, batch, g.H, g.W, p.ldo32,
+               g.ge, (int)filters, reinterpret_cast<uint32_t*>(out));
+      rc = launched();
+    }
+    cudaFreeAsync(scratch, st);
+  }
+  return rc;
+}
+
 inline void pack_args(Args& g, const b2_thresh& th, uint64_t* out, int64_t n) {
   g.out_bits = reinterpret_cast<uint32_t*>(out);
   g.ldo32 = 2 * wpl64(n);
@@ -476,6 +561,10 @@ int conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, cons
   const int64_t k = (int64_t)kh * kw * c;
   g.N = (int)filters;
   pack_args(g, th, out, filters);
+  if constexpr (F4) {
+    if (batch && !splitk_count<A_CONV, E_PACK>(g, k) && padrow_ok(g, c, filters, k, batch))
+      return padrow_launch(g, lines, batch, c, w_i8, filters, k, pool, out, S(stream));
+  }
   if (pool) return launch<A_CONV, E_POOLPACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
   return launch<A_CONV, E_PACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
 }

@@ -107,6 +107,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// Wait for roles that are not on the MMA's critical path: the thread is
+// suspended in hardware until the phase completes (or the hint expires)
+// instead of polling, so it does not take issue slots from the MMA thread
+// and the producers sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!done);
+}
+
+#ifndef B2_SUSPEND  // 1: TMA, producer and epilogue waits suspend in hardware (the MMA thread polls)
+#define B2_SUSPEND 0
+#endif
+__device__ __forceinline__ void mbar_wait_nc(uint64_t* bar, uint32_t parity) {
+  if constexpr (B2_SUSPEND)
+    mbar_wait_suspend(bar, parity);
+  else
+    mbar_wait(bar, parity);
+}
+
 // Same wait for roles that idle for long stretches (epilogue, TMA issue):
 // back off so their polling does not steal issue slots from the producers.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
@@ -803,7 +830,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         int kb0, kb1;
         item_krange(g, ksp, t, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_nc(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], B_STAGE_BYTES);
 #pragma unroll
           for (int at = 0; at < (F4 ? BKS / 256 : BKS / BK); ++at)  // one 128-byte-wide box per swizzle atom
@@ -890,7 +917,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       if constexpr (F4) {
         // fp4: this thread's WPH words of the stage are WPH 16-byte chunks of
         // its row in the shared-memory A stage (128-byte swizzle, K-major)
-        mbar_wait(&empty[stage], ph ^ 1);
+        mbar_wait_nc(&empty[stage], ph ^ 1);
         uint8_t* row = sa + stage * A_STAGE_BYTES + r * 128;
         // one K stage per tile (the first conv): only the words its klast
         // K=64 MMAs read are stored
@@ -913,7 +940,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[pending]);
       }
-      mbar_wait(&empty[stage], ph ^ 1);
+      mbar_wait_nc(&empty[stage], ph ^ 1);
       tc_fence_after();
 #ifndef B2_PROBE_SKIP_A
       if constexpr (WPH == 8) {
@@ -1170,7 +1197,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #ifdef B2_EPI_SLEEP
       mbar_wait_sleep(&tfull[acc], aph, B2_EPI_SLEEP);
 #else
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait_nc(&tfull[acc], aph);
 #endif
       tc_fence_after();
       uint32_t words[ECH];

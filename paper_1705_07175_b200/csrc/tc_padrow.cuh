@@ -1,0 +1,308 @@
+// Padded-row implicit GEMM for stride-1 "same" convolutions on the fp4
+// tensor cores (tcgen05.mma kind::mxf4).
+//
+// The im2col producers of k_tc_gemm expand every input word once per window
+// cell (9x for 3x3).  Here the output pixels are laid out on a VIRTUAL grid
+// whose rows are W + 1 wide (one shared zero column) and whose images are
+// H + 1 rows tall (one shared zero row): v(n, y, x) = n (H+1)(W+1) + y (W+1)
+// + x.  The input of window cell (dy, dx) for output v is then v + dy (W+1)
+// + dx for EVERY v, so one expanded copy of the input band (the virtual rows
+// a 128-row tile touches, ±(W+2)) serves all cells: cell (dy, dx) is an MMA
+// descriptor whose start is shifted by that many rows.  The band uses the
+// no-swizzle K-major canonical layout (8-row x 16-byte core matrices, rows
+// 16 bytes apart, one 16-byte K plane per input word), in which a shift by
+// any number of rows is a plain start-address offset.
+//
+// Virtual rows at the zero column / zero row produce accumulators that are
+// discarded (W=32: 9.6 % of the MMA work).  A 2x2 pool window spans rows v
+// and v + W + 1, which may sit in different tiles, so pooled layers write
+// the thresholded bits unpooled and k_pool_bits combines each window (OR for
+// ge channels, AND for le: exact, the threshold is monotone).
+//
+// Scope: fp4, c % 128 == 0, N <= 128 (one 128-column tile), weights
+// resident in shared memory (K <= 1536), odd square-or-not windows with
+// pad = (k - 1) / 2, stride 1.
+#pragma once
+#include "tc_i8.cuh"
+
+namespace b2 {
+namespace tc {
+
+struct PadArgs {
+  const uint32_t* x;   // NHWC-bits input, sstride words per pixel
+  int N, H, W, sstride, P;  // P = c / 32 words (= K planes) per pixel
+  int kh, kw, pad;
+  int Wp;              // W + 1
+  int64_t VI, Vtotal;  // virtual rows per image, in all
+  int R8;              // band rows (multiple of 8)
+  int nkb;             // 128-byte B atoms (256 K elements) in shared memory
+  int F;               // filters (<= 128)
+  int kmmas;           // K=64 MMAs per window cell (= P / 2)
+  uint32_t* out_bits;  // (N*H*W, ldo32) words
+  int64_t ldo32;
+  const int32_t* thresh;
+  const uint8_t* ge;
+};
+
+#ifndef B2_PADROW_LBO_K
+#define B2_PADROW_LBO_K 1  // 1: LBO = K-plane stride, SBO = 8-row group stride (0: swapped)
+#endif
+
+// K-major, no swizzle: 8-row x 16-byte core matrices
+__device__ __forceinline__ uint64_t noswz_desc(uint32_t saddr, uint32_t kplane_bytes) {
+  const uint64_t lbo = B2_PADROW_LBO_K ? kplane_bytes : 128u, sbo = B2_PADROW_LBO_K ? 128u : kplane_bytes;
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+constexpr int PR_NPW = 8;       // producer warps
+constexpr int PR_NEPI = 4;      // epilogue warps
+constexpr int PR_BANDS = 4;     // band ring (tiles in flight: hides the band loads' DRAM latency)
+constexpr int PR_ACC = 3;       // accumulator buffers (3 x 128 columns + scale columns)
+constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot
+
+__global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
+    k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
+  constexpr int BN = 128;
+  constexpr uint32_t IDESC = idesc_f4(BN);
+  constexpr int EPI0 = 4 + PR_NPW;
+  constexpr int ACC_COLS = BN;
+  constexpr int SF_COL = PR_ACC * ACC_COLS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sb = smem;                                    // resident weights: nkb atoms of BN x 128 B
+  uint8_t* sband = sb + g.nkb * BN * 128;                // PR_BANDS x PR_BAND_MAX
+  int4* sthr = reinterpret_cast<int4*>(sband + PR_BANDS * PR_BAND_MAX);  // 64 x (mul, add) pairs
+  uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + BN / 2);
+  uint64_t* bres = reinterpret_cast<uint64_t*>(sgm + BN / 32);
+  uint64_t* bfull = bres + 1;
+  uint64_t* bempty = bfull + PR_BANDS;
+  uint64_t* tfull = bempty + PR_BANDS;
+  uint64_t* tempty = tfull + PR_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + PR_ACC);
+  uint2* soff = reinterpret_cast<uint2*>(tmem_slot + 2);  // per MMA: (A, B) descriptor address offsets (16 B units)
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles = (g.Vtotal + BM - 1) / BM;
+  const uint32_t plane_bytes = (uint32_t)g.R8 * 16u;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(bres, 1);
+    for (int b = 0; b < PR_BANDS; ++b) {
+      mbar_init(&bfull[b], PR_NPW);
+      mbar_init(&bempty[b], 1);
+    }
+    for (int a = 0; a < PR_ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], PR_NEPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp < 4) {  // unit block scales
+    uint32_t ones[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) ones[i] = 0x7F7F7F7Fu;
+    tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + SF_COL, ones);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_entry();
+
+  if (warp == 0) {
+    // ------------------------------------------------ weights, once
+    if (lane == 0) {
+      mbar_expect_tx(bres, (uint32_t)g.nkb * BN * 128);
+      for (int a = 0; a < g.nkb; ++a) tma_load_2d(sb + a * BN * 128, &bmap, bres, a * 128, 0);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // descriptor offsets of every MMA of a tile, once: (window cell, K chunk)
+      // -> band plane + row shift for A, weight atom + 32-byte step for B
+      int nmma = 0;
+      for (int cy = 0; cy < g.kh; ++cy)
+        for (int cx = 0; cx < g.kw; ++cx) {
+          const int off = (g.Wp + 1) + (cy - g.pad) * g.Wp + (cx - g.pad);  // band row of tile row 0
+          const int cell = cy * g.kw + cx;
+          for (int kc = 0; kc < g.kmmas; ++kc, ++nmma) {
+            const int k = cell * g.P * 32 + kc * 64;  // K element
+            soff[nmma] = make_uint2(((uint32_t)(2 * kc) * plane_bytes + (uint32_t)off * 16u) >> 4,
+                                    (uint32_t)((k >> 8) * BN * 128 + ((k & 255) >> 6) * 32) >> 4);
+          }
+        }
+      mbar_wait(bres, 0);
+      int slot = 0, acc = 0;
+      uint32_t bph = 0, aph = 0;
+      const uint64_t bdesc0 = sw128_desc(smem_u32(sb));
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(&bfull[slot], bph);
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * ACC_COLS;
+        const uint64_t adesc0 = noswz_desc(smem_u32(sband + slot * PR_BAND_MAX), plane_bytes);
+        for (int i = 0; i < nmma; ++i) {
+          const uint2 o = soff[i];
+          tc_mma_f4(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
+        }
+        tc_commit(&bempty[slot]);
+        tc_commit(&tfull[acc]);
+        if (++slot == PR_BANDS) slot = 0, bph ^= 1;
+        if (++acc == PR_ACC) acc = 0, aph ^= 1;
+      }
+    }
+  } else if (warp >= 4 && warp < EPI0) {
+    // ------------------------------------------------ band producers
+    // each thread owns up to UMAX (band row, 4-word group) units per tile;
+    // a tile's loads are issued before waiting for its band slot
+    constexpr int UMAX = 2;
+    const int pt = (warp - 4) * 32 + lane;  // 0 .. 255
+    const int groups = g.P / 4;             // 4-word groups per pixel
+    const int units = g.R8 * groups;
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int64_t v0 = t * BM - (g.Wp + 1);
+      uint4 w[UMAX];
+      bool ok[UMAX];
+#pragma unroll
+      for (int i = 0; i < UMAX; ++i) {
+        const int u = pt + i * 32 * PR_NPW;
+        ok[i] = false;
+        w[i] = make_uint4(0, 0, 0, 0);
+        if (u < units) {
+          const int b = u / groups, grp = u - b * groups;
+          const int64_t v = v0 + b;
+          if (v >= 0 && v < g.Vtotal) {
+            const int64_t n = v / g.VI;
+            const int rem = (int)(v - n * g.VI);
+            const int y = rem / g.Wp, x = rem - y * g.Wp;
+            if (y < g.H && x < g.W) {
+              ok[i] = true;
+              w[i] = __ldg(reinterpret_cast<const uint4*>(g.x + ((n * g.H + y) * g.W + x) * g.sstride + 4 * grp));
+            }
+          }
+        }
+      }
+      mbar_wait_suspend(&bempty[slot], ph ^ 1);
+      uint8_t* band = sband + slot * PR_BAND_MAX;
+#pragma unroll
+      for (int i = 0; i < UMAX; ++i) {
+        const int u = pt + i * 32 * PR_NPW;
+        if (u < units) {
+          const int b = u / groups, grp = u - b * groups;
+          uint32_t o[16];
+          widen_f4(w[i].x, ok[i], o);
+          widen_f4(w[i].y, ok[i], o + 4);
+          widen_f4(w[i].z, ok[i], o + 8);
+          widen_f4(w[i].w, ok[i], o + 12);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(band + (size_t)(4 * grp + j) * plane_bytes + (size_t)b * 16) =
+                make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bfull[slot]);
+      if (++slot == PR_BANDS) slot = 0, ph ^= 1;
+    }
+  } else if (warp >= EPI0) {
+    // ------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int et = (warp - EPI0) * 32 + lane;
+    {
+      Args ga{};
+      ga.N = g.F;
+      ga.thresh = g.thresh;
+      ga.ge = g.ge;
+      stage_thresholds<true>(ga, 0, BN, et, 32 * PR_NEPI, lane, sthr, sgm);
+    }
+    epi_bar<PR_NEPI>();
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      mbar_wait_suspend(&tfull[acc], aph);
+      tc_fence_after();
+      uint32_t words[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS + c * 32, v);
+        tmem_wait_ld();
+        words[c] = thr_word<true>(v, sthr + c * 16);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      const int64_t v = t * BM + r;
+      if (v < g.Vtotal) {
+        const int64_t n = v / g.VI;
+        const int rem = (int)(v - n * g.VI);
+        const int y = rem / g.Wp, x = rem - y * g.Wp;
+        if (y < g.H && x < g.W) {
+          uint32_t* o = g.out_bits + ((n * g.H + y) * g.W + x) * g.ldo32;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < g.ldo32) o[c] = words[c];
+        }
+      }
+      if (++acc == PR_ACC) acc = 0, aph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+inline int padrow_smem_bytes(int nkb) {
+  return nkb * 128 * 128 + PR_BANDS * PR_BAND_MAX + 64 * 16 + 16 + 8 * (1 + 2 * PR_BANDS + 2 * PR_ACC) + 16 +
+         8 * 128 + 1024;  // + MMA offset table (kh*kw*kmmas <= 128)
+}
+
+// 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for
+// ge channels, AND for le channels (max(v) >= t <=> OR(v_i >= t); max(v) <= t
+// <=> AND(v_i <= t)).  One thread per output word.
+__global__ void __launch_bounds__(256) k_pool_bits(const uint32_t* __restrict__ in, int64_t n_img, int h, int w,
+                                                   int64_t ldo32, const uint8_t* __restrict__ ge, int c,
+                                                   uint32_t* __restrict__ out) {
+  pdl_entry();
+  __shared__ uint32_t sgm[64];  // ge masks, one word per 32 channels (ldo32 <= 64)
+  for (int base = 0; base < (int)ldo32 * 32; base += 256) {
+    const int ch = base + (int)threadIdx.x;
+    const uint32_t m = __ballot_sync(0xffffffffu, ch < c && __ldg(ge + (ch < c ? ch : 0)) != 0);
+    if ((threadIdx.x & 31) == 0 && (ch >> 5) < 64) sgm[ch >> 5] = m;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int hp = h / 2, wp = w / 2;
+  const int64_t total = n_img * hp * wp * ldo32;
+  if (i >= total) return;
+  const int wd = (int)(i % ldo32);
+  const int64_t site = i / ldo32;
+  const int64_t n = site / (hp * wp);
+  const int rem = (int)(site - n * hp * wp);
+  const int py = rem / wp, px = rem - py * wp;
+  const uint32_t gm = sgm[wd];
+  const int64_t s00 = (n * h + 2 * py) * w + 2 * px;
+  const uint32_t a = __ldg(in + s00 * ldo32 + wd), b = __ldg(in + (s00 + 1) * ldo32 + wd);
+  const uint32_t c2 = __ldg(in + (s00 + w) * ldo32 + wd), d = __ldg(in + (s00 + w + 1) * ldo32 + wd);
+  out[i] = ((a | b | c2 | d) & gm) | ((a & b & c2 & d) & ~gm);
+}
+
+}  // namespace tc
+}  // namespace b2
