@@ -86,7 +86,11 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
                                                 (6, 6, 64, 200, True, 3),
                                                 (4, 4, 512, 512, True, 1), (8, 8, 512, 200, False, 3),
                                                 (6, 6, 512, 130, True, 2), (8, 8, 1024, 64, False, 1),
-                                                (2, 2, 512, 2048, True, 1)])
+                                                (2, 2, 512, 2048, True, 1),
+                                                # fp4 padded-row implicit GEMM (>= 128 x 148 virtual rows,
+                                                # <= 128 filters): pooled, unpooled, ragged filter count
+                                                (32, 32, 128, 128, True, 20), (16, 16, 128, 64, False, 80),
+                                                (8, 8, 128, 100, True, 240)])
 def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch, fmt):
     rng = np.random.default_rng(5 + h + c + f)
     xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
