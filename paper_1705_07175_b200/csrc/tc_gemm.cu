@@ -428,6 +428,8 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   p.Wp = g.W + 1;
   p.VI = (int64_t)(g.H + 1) * p.Wp;
   p.Vtotal = p.VI * batch;
+  p.vi_magic = ~0ull / (uint64_t)p.VI + 1;  // ceil(2^64 / VI), exact multiply-high division for v < 2^40
+  p.wp_magic = (uint32_t)((((uint64_t)1 << 32) + p.Wp - 1) / p.Wp);
   p.R8 = ((2 * p.Wp + 2 + BM) + 7) / 8 * 8;
   p.nkb = (int)((k + 255) / 256);
   p.F = (int)filters;

@@ -34,6 +34,8 @@ struct PadArgs {
   int kh, kw, pad;
   int Wp;              // W + 1
   int64_t VI, Vtotal;  // virtual rows per image, in all
+  uint64_t vi_magic;   // ceil(2^64 / VI): image of a virtual row by one multiply-high
+  uint32_t wp_magic;   // ceil(2^32 / Wp): row within the image
   int R8;              // band rows (multiple of 8)
   int nkb;             // 128-byte B atoms (256 K elements) in shared memory
   int F;               // filters (<= 128)
@@ -55,8 +57,22 @@ __device__ __forceinline__ uint64_t noswz_desc(uint32_t saddr, uint32_t kplane_b
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
+// virtual row v -> (image n, row y, column x) of the padded grid
+__device__ __forceinline__ void vsplit(const PadArgs& g, int64_t v, int64_t& n, int& y, int& x) {
+  n = (int64_t)__umul64hi((uint64_t)v, g.vi_magic);
+  const uint32_t rem = (uint32_t)(v - n * g.VI);
+  y = (int)__umulhi(rem, g.wp_magic);
+  x = (int)rem - y * g.Wp;
+}
+
 constexpr int PR_NPW = 8;       // producer warps
-constexpr int PR_NEPI = 4;      // epilogue warps
+#ifndef B2_PR_EPI_SUSPEND  // epilogue waits: 1 suspend in hardware, 0 poll
+#define B2_PR_EPI_SUSPEND 0
+#endif
+#ifndef B2_PR_NEPI
+#define B2_PR_NEPI 4
+#endif
+constexpr int PR_NEPI = B2_PR_NEPI;  // epilogue warps: 4 (one per lane quarter) or 8 (two, half the columns each)
 constexpr int PR_BANDS = 4;     // band ring (tiles in flight: hides the band loads' DRAM latency)
 constexpr int PR_ACC = 3;       // accumulator buffers (3 x 128 columns + scale columns)
 constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot
@@ -184,9 +200,9 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
           const int b = u / groups, grp = u - b * groups;
           const int64_t v = v0 + b;
           if (v >= 0 && v < g.Vtotal) {
-            const int64_t n = v / g.VI;
-            const int rem = (int)(v - n * g.VI);
-            const int y = rem / g.Wp, x = rem - y * g.Wp;
+            int64_t n;
+            int y, x;
+            vsplit(g, v, n, y, x);
             if (y < g.H && x < g.W) {
               ok[i] = true;
               w[i] = __ldg(reinterpret_cast<const uint4*>(g.x + ((n * g.H + y) * g.W + x) * g.sstride + 4 * grp));
@@ -222,6 +238,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const int et = (warp - EPI0) * 32 + lane;
+    constexpr int ECH = 4 / (PR_NEPI / 4);        // 32-column chunks per epilogue warp
+    const int c0 = ((warp - EPI0) >> 2) * ECH;    // first chunk of this warp
     {
       Args ga{};
       ga.N = g.F;
@@ -233,29 +251,39 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
     int acc = 0;
     uint32_t aph = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+#if B2_PR_EPI_SUSPEND
       mbar_wait_suspend(&tfull[acc], aph);
+#else
+      mbar_wait(&tfull[acc], aph);
+#endif
       tc_fence_after();
-      uint32_t words[4];
+      uint32_t words[ECH];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS + c0 * 32;
+      // software-pipelined: chunk c + 1 is in flight while chunk c is thresholded
+      uint32_t va[32], vb[32];
+      tmem_ld32(ta, va);
+      tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS + c * 32, v);
-        tmem_wait_ld();
-        words[c] = thr_word<true>(v, sthr + c * 16);
+      for (int c = 0; c < ECH; ++c) {
+        uint32_t(&v)[32] = (c & 1) ? vb : va;
+        uint32_t(&vn)[32] = (c & 1) ? va : vb;
+        if (c + 1 < ECH) tmem_ld32(ta + (c + 1) * 32, vn);
+        words[c] = thr_word<true>(v, sthr + (c0 + c) * 16);
+        if (c + 1 < ECH) tmem_wait_ld();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       const int64_t v = t * BM + r;
       if (v < g.Vtotal) {
-        const int64_t n = v / g.VI;
-        const int rem = (int)(v - n * g.VI);
-        const int y = rem / g.Wp, x = rem - y * g.Wp;
+        int64_t n;
+        int y, x;
+        vsplit(g, v, n, y, x);
         if (y < g.H && x < g.W) {
           uint32_t* o = g.out_bits + ((n * g.H + y) * g.W + x) * g.ldo32;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (c < g.ldo32) o[c] = words[c];
+          for (int c = 0; c < ECH; ++c)
+            if (c0 + c < g.ldo32) o[c0 + c] = words[c];
         }
       }
       if (++acc == PR_ACC) acc = 0, aph ^= 1;

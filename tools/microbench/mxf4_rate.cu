@@ -21,7 +21,14 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int n) {
   return (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
 }
 
-template <int N, int KIND, bool W>  // KIND 0: i8 (A tmem), 1: mxf4 SS
+// K-major, no swizzle: 8-row x 16-byte core matrices, SBO = 128 B between
+// 8-row groups, LBO = K-plane stride (the padded-row conv's band layout)
+__device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+template <int N, int KIND, bool W>  // KIND 0: i8 (A tmem), 1: mxf4 SS, 2: mxf4 SS with A no-swizzle
 __global__ void k(int iters, long long* clk, float* check) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t slot;
@@ -73,7 +80,9 @@ __global__ void k(int iters, long long* clk, float* check) {
         asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(
                          tm), "r"(tm + 300 + (i & 3) * 8), "l"(bd), "r"(idesc_i8(N)), "r"(i));
       } else {
-        const uint64_t ad = desc(sbase + 32768 + (i & 3) * 32);
+        // KIND 2: A rows 16 B apart per K plane (planes 2048 B apart), shifted by i % 7 rows
+        const uint64_t ad = KIND == 2 ? desc_noswz(sbase + 32768 + (i % 7) * 16, 2048, 128)
+                                      : desc(sbase + 32768 + (i & 3) * 32);
         asm volatile(
             "{.reg .pred p; setp.ne.b32 p, %4, 0; "
             "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;}" ::"r"(tm),
@@ -137,7 +146,7 @@ void run(long long* d, float* chk) {
   double macs = (double)iters * 128 * N * kk;
   printf("{\"mma\": \"%s M=128 N=%d K=%d\", \"smem_store_traffic\": %d, \"clk_per_mma\": %.1f, \"mac_per_clk_per_sm\": %.0f, "
          "\"acc_row0\": %.1f, \"acc_row127\": %.1f, \"expect\": %d, \"store_B_per_clk\": %.1f, \"err\": \"%s\"}\n",
-         KIND ? "mxf4 SS" : "i8 TS", N, kk, (int)W, avg / iters, macs / avg, h[0], h[127], iters * kk, h[128] / avg,
+         KIND == 2 ? "mxf4 SS, A no-swizzle" : (KIND ? "mxf4 SS" : "i8 TS"), N, kk, (int)W, avg / iters, macs / avg, h[0], h[127], iters * kk, h[128] / avg,
          cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -153,5 +162,7 @@ int main() {
   run<128, 1, true>(d, chk);
   run<256, 1, true>(d, chk);
   run<128, 0, true>(d, chk);
+  run<128, 2, false>(d, chk);
+  run<256, 2, false>(d, chk);
   return 0;
 }
