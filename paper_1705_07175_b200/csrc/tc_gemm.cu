@@ -471,7 +471,7 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   int rc = launched();
   if (pool) {
     if (!rc) {
-      const int64_t n = batch * (g.H / 2) * (g.W / 2) * p.ldo32;
+      const int64_t n = batch * (g.H / 2) * (g.W / 2);  // pooled sites
       launch_k(k_pool_bits, (unsigned)cdiv(n, 256), 256, 0, st, (const uint32_t*)scratch, batch, g.H, g.W, p.ldo32,
                g.ge, (int)filters, reinterpret_cast<uint32_t*>(out));
       rc = launched();

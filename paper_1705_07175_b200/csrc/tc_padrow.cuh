@@ -304,7 +304,8 @@ inline int padrow_smem_bytes(int nkb) {
 
 // 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for
 // ge channels, AND for le channels (max(v) >= t <=> OR(v_i >= t); max(v) <= t
-// <=> AND(v_i <= t)).  One thread per output word.
+// <=> AND(v_i <= t)).  One thread per pooled site (all its words; 16-byte
+// accesses when a line is 4 words).
 __global__ void __launch_bounds__(256) k_pool_bits(const uint32_t* __restrict__ in, int64_t n_img, int h, int w,
                                                    int64_t ldo32, const uint8_t* __restrict__ ge, int c,
                                                    uint32_t* __restrict__ out) {
@@ -316,20 +317,31 @@ __global__ void __launch_bounds__(256) k_pool_bits(const uint32_t* __restrict__ 
     if ((threadIdx.x & 31) == 0 && (ch >> 5) < 64) sgm[ch >> 5] = m;
   }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t site = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int hp = h / 2, wp = w / 2;
-  const int64_t total = n_img * hp * wp * ldo32;
-  if (i >= total) return;
-  const int wd = (int)(i % ldo32);
-  const int64_t site = i / ldo32;
+  if (site >= n_img * hp * wp) return;
   const int64_t n = site / (hp * wp);
   const int rem = (int)(site - n * hp * wp);
   const int py = rem / wp, px = rem - py * wp;
-  const uint32_t gm = sgm[wd];
   const int64_t s00 = (n * h + 2 * py) * w + 2 * px;
-  const uint32_t a = __ldg(in + s00 * ldo32 + wd), b = __ldg(in + (s00 + 1) * ldo32 + wd);
-  const uint32_t c2 = __ldg(in + (s00 + w) * ldo32 + wd), d = __ldg(in + (s00 + w + 1) * ldo32 + wd);
-  out[i] = ((a | b | c2 | d) & gm) | ((a & b & c2 & d) & ~gm);
+  const uint32_t* p0 = in + s00 * ldo32;
+  const uint32_t* p1 = in + (s00 + w) * ldo32;
+  uint32_t* o = out + site * ldo32;
+  if (ldo32 == 4) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p0)), b = __ldg(reinterpret_cast<const uint4*>(p0 + 4));
+    const uint4 c2 = __ldg(reinterpret_cast<const uint4*>(p1)), d = __ldg(reinterpret_cast<const uint4*>(p1 + 4));
+    auto f = [&](uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t gm) {
+      return ((x0 | x1 | x2 | x3) & gm) | ((x0 & x1 & x2 & x3) & ~gm);
+    };
+    *reinterpret_cast<uint4*>(o) = make_uint4(f(a.x, b.x, c2.x, d.x, sgm[0]), f(a.y, b.y, c2.y, d.y, sgm[1]),
+                                              f(a.z, b.z, c2.z, d.z, sgm[2]), f(a.w, b.w, c2.w, d.w, sgm[3]));
+    return;
+  }
+  for (int wd = 0; wd < (int)ldo32; ++wd) {
+    const uint32_t gm = sgm[wd];
+    const uint32_t a = __ldg(p0 + wd), b = __ldg(p0 + ldo32 + wd), c2 = __ldg(p1 + wd), d = __ldg(p1 + ldo32 + wd);
+    o[wd] = ((a | b | c2 | d) & gm) | ((a & b & c2 & d) & ~gm);
+  }
 }
 
 }  // namespace tc
