@@ -371,8 +371,12 @@ inline int64_t kpad_for(int64_t k) { return F4 ? kpad_f4(k) : kpad_of(k); }
 static_assert(KPAD % 128 == 0, "weight rows pad to whole TMA boxes");
 
 inline bool conv_ok(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad) {
-  return batch >= 0 && h >= 1 && w >= 1 && c >= 1 && filters >= 1 && filters <= INT32_MAX && kh >= 1 && kw >= 1 &&
-         stride >= 1 && pad >= 0 && h + 2 * pad >= kh && w + 2 * pad >= kw;
+  if (!(batch >= 0 && h >= 1 && w >= 1 && c >= 1 && filters >= 1 && filters <= INT32_MAX && kh >= 1 && kw >= 1 &&
+        stride >= 1 && pad >= 0 && h + 2 * pad >= kh && w + 2 * pad >= kw))
+    return false;
+  // output rows (and pool-window rows) are indexed in 32 bits on the device
+  const int64_t ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  return batch * ho * wo < ((int64_t)1 << 31);
 }
 
 inline void conv_args(Args& g, const void* x, int64_t batch, int h, int w, int c, int kh, int kw, int stride,

@@ -274,22 +274,38 @@ __host__ __device__ __forceinline__ int perm_pos(int k) {  // element k of a 32-
 
 // Output row -> (image, oy, ox); pool-ordered rows put each 2x2 window in
 // four consecutive rows: m = 4*q + 2*cy + cx.
+// 32-bit arithmetic: the conv entry points require M < 2^31.
 template <bool POOLED>
 __device__ __forceinline__ void row_pos(const Args& g, int64_t m, int64_t& img, int& oy, int& ox) {
+  const uint32_t mm = (uint32_t)m;
   if constexpr (POOLED) {
-    int64_t q = m >> 2;
-    int cell = (int)(m & 3);
-    int hp = g.Ho >> 1, wp = g.Wo >> 1;
-    img = q / (hp * wp);
-    int r = (int)(q - img * (hp * wp));
-    oy = 2 * (r / wp) + (cell >> 1);
-    ox = 2 * (r % wp) + (cell & 1);
+    const uint32_t q = mm >> 2;
+    const uint32_t cell = mm & 3u;
+    const uint32_t hp = (uint32_t)g.Ho >> 1, wp = (uint32_t)g.Wo >> 1;
+    const uint32_t im = q / (hp * wp);
+    const uint32_t r = q - im * (hp * wp);
+    const uint32_t ry = r / wp;
+    img = im;
+    oy = (int)(2 * ry + (cell >> 1));
+    ox = (int)(2 * (r - ry * wp) + (cell & 1));
   } else {
-    int64_t hw = (int64_t)g.Ho * g.Wo;
-    img = m / hw;
-    int r = (int)(m - img * hw);
-    oy = r / g.Wo;
-    ox = r % g.Wo;
+    const uint32_t hw = (uint32_t)g.Ho * (uint32_t)g.Wo;
+    const uint32_t im = mm / hw;
+    const uint32_t r = mm - im * hw;
+    const uint32_t y = r / (uint32_t)g.Wo;
+    img = im;
+    oy = (int)y;
+    ox = (int)(r - y * (uint32_t)g.Wo);
+  }
+}
+
+// persistent tile loops advance t by the grid size: keep (m tile, n tile)
+// incrementally, dividing only when the m index wraps
+__device__ __forceinline__ void next_tile(int64_t& mt, int64_t& nt, int64_t step, int64_t mtiles) {
+  mt += step;
+  if (mt >= mtiles) {
+    nt += mt / mtiles;
+    mt %= mtiles;
   }
 }
 
@@ -357,6 +373,7 @@ __device__ __forceinline__ uint32_t div_magic(uint32_t n, uint64_t magic) {  // 
 template <int AM, bool POOLED, int WS, int TW, bool DIRECT = false>  // WS = K words per stage, TW = words per producer thread
 struct ACursor {
   int64_t t;       // work item of the next fetch (tile t / ksp)
+  int64_t mt, nt_; // m (and n) tile of t, kept incrementally when ksp == 1
   int kb, kend;    // K block of the next fetch, end of the item's K range
   bool mok;        // row inside M
   const uint32_t* base;
@@ -367,7 +384,7 @@ struct ACursor {
   __device__ __forceinline__ void tile_setup(const Args& g, int64_t mtiles, int64_t tiles, int r, int half,
                                              int ksp) {
     item_krange(g, ksp, t, kb, kend);
-    const int64_t m = (t / ksp % mtiles) * BM + r;
+    const int64_t m = mt * BM + r;
     mok = t < tiles * ksp && m < g.M;
     if constexpr (AM == A_CONV) {
       img = 0;
@@ -392,12 +409,18 @@ struct ACursor {
   __device__ __forceinline__ void start(const Args& g, int64_t t0, int64_t mtiles, int64_t tiles, int r, int half,
                                         int ksp) {
     t = t0;
+    mt = (t0 / ksp) % mtiles;
+    nt_ = 0;
     tile_setup(g, mtiles, tiles, r, half, ksp);
   }
   __device__ __forceinline__ void advance(const Args& g, int64_t step, int64_t mtiles, int64_t tiles, int r,
                                           int half, int ksp) {
     if (++kb == kend) {
       t += step;
+      if (ksp == 1)
+        next_tile(mt, nt_, step, mtiles);
+      else
+        mt = (t / ksp) % mtiles;
       tile_setup(g, mtiles, tiles, r, half, ksp);
     } else if constexpr (AM == A_CONV && !DIRECT) {
       within += WS;
@@ -1182,9 +1205,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           g.out_bits[(POOLED ? (m >> 2) : m) * g.ldo32 + wcol] = w;
       }
     } else
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int64_t m = (t % mtiles) * BM + r;
-      const int n0 = (int)(t / mtiles) * BN;
+    for (int64_t t = blockIdx.x, mt = blockIdx.x % mtiles, nt = blockIdx.x / mtiles; t < tiles;
+         t += gridDim.x, next_tile(mt, nt, gridDim.x, mtiles)) {
+      const int64_t m = mt * BM + r;
+      const int n0 = (int)nt * BN;
       const int tcol = static_thr ? n0 : 0;  // table column of this tile's first column
       const bool mok = m < g.M;
       if constexpr (EM == E_PACK || EM == E_POOLPACK) {
