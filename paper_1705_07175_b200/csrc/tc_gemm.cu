@@ -447,8 +447,10 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   CUtensorMap map;
   if (int rc = make_bmap(&map, w_f4, filters, kpad_f4(k) / 2, 128)) return rc;
   const int smem = padrow_smem_bytes(p.nkb);
-  static std::atomic<uint64_t> attr{0};
-  smem_optin(k_padrow_conv, smem, attr);
+  const bool k33 = g.kh == 3 && p.kmmas == 2;  // 3x3, c = 128: the unrolled issue loop
+  auto kern = k33 ? k_padrow_conv<3, 2> : k_padrow_conv<0, 0>;
+  static std::atomic<uint64_t> attr33{0}, attr0{0};
+  smem_optin(kern, smem, k33 ? attr33 : attr0);
   const int64_t tiles = (p.Vtotal + BM - 1) / BM;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
   void* scratch = nullptr;
@@ -471,7 +473,7 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   } else {
     p.out_bits = reinterpret_cast<uint32_t*>(out);
   }
-  launch_k(k_padrow_conv, grid, 32 * (4 + PR_NPW + PR_NEPI), smem, st, map, p);
+  launch_k(kern, grid, 32 * (4 + PR_NPW + PR_NEPI), smem, st, map, p);
   int rc = launched();
   if (pool) {
     if (!rc) {

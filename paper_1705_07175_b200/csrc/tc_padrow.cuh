@@ -23,6 +23,8 @@
 // resident in shared memory (K <= 1536), odd square-or-not windows with
 // pad = (k - 1) / 2, stride 1.
 #pragma once
+#include <cstdio>
+
 #include "tc_i8.cuh"
 
 namespace b2 {
@@ -77,6 +79,11 @@ constexpr int PR_BANDS = 4;     // band ring (tiles in flight: hides the band lo
 constexpr int PR_ACC = 3;       // accumulator buffers (3 x 128 columns + scale columns)
 constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot
 
+// KH, KMMAS > 0: compile-time window and K chunks per cell (the issuing
+// thread's 18 descriptor offsets for 3x3 / c = 128 stay in registers and the
+// MMA loop is fully unrolled: a runtime loop reading them from shared memory
+// issued one MMA per ~113 cycles, slower than the 64-cycle MMA itself)
+template <int KH, int KMMAS>
 __global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
     k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
   constexpr int BN = 128;
@@ -161,21 +168,60 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
       int slot = 0, acc = 0;
       uint32_t bph = 0, aph = 0;
       const uint64_t bdesc0 = sw128_desc(smem_u32(sb));
+#ifdef B2_PR_TIMING
+      long long c_band = 0, c_acc = 0, c_issue = 0, c_t0 = clock64();
+#endif
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+#ifdef B2_PR_TIMING
+        long long c0 = clock64();
+#endif
         mbar_wait(&bfull[slot], bph);
+#ifdef B2_PR_TIMING
+        long long c1 = clock64();
+#endif
         mbar_wait(&tempty[acc], aph ^ 1);
+#ifdef B2_PR_TIMING
+        long long c2 = clock64();
+        c_band += c1 - c0, c_acc += c2 - c1;
+#endif
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
         const uint64_t adesc0 = noswz_desc(smem_u32(sband + slot * PR_BAND_MAX), plane_bytes);
-        for (int i = 0; i < nmma; ++i) {
-          const uint2 o = soff[i];
-          tc_mma_f4(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
+        if constexpr (KH > 0) {
+          constexpr int PAD = KH / 2;
+#pragma unroll
+          for (int cy = 0; cy < KH; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < KH; ++cx)
+#pragma unroll
+              for (int kc = 0; kc < KMMAS; ++kc) {
+                const int cell = cy * KH + cx;
+                const int k = (cell * KMMAS + kc) * 64;  // K element (c = 32 * 2 * KMMAS)
+                const uint32_t off = (uint32_t)((g.Wp + 1) + (cy - PAD) * g.Wp + (cx - PAD));
+                const uint32_t ao = ((uint32_t)(2 * kc) * plane_bytes + off * 16u) >> 4;
+                const uint32_t bo = (uint32_t)((k >> 8) * BN * 128 + ((k & 255) >> 6) * 32) >> 4;
+                tc_mma_f4(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
+                          (cell | kc) ? 1u : 0u);
+              }
+        } else {
+          for (int i = 0; i < nmma; ++i) {
+            const uint2 o = soff[i];
+            tc_mma_f4(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
+          }
         }
+#ifdef B2_PR_TIMING
+        c_issue += clock64() - c2;
+#endif
         tc_commit(&bempty[slot]);
         tc_commit(&tfull[acc]);
         if (++slot == PR_BANDS) slot = 0, bph ^= 1;
         if (++acc == PR_ACC) acc = 0, aph ^= 1;
       }
+#ifdef B2_PR_TIMING
+      if (blockIdx.x < 3)
+        printf("cta %d: total %lld  wait band %lld  wait acc %lld  issue %lld  tiles %lld\n", blockIdx.x,
+               clock64() - c_t0, c_band, c_acc, c_issue, (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+#endif
     }
   } else if (warp >= 4 && warp < EPI0) {
     // ------------------------------------------------ band producers
