@@ -411,7 +411,7 @@ inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t 
     return e ? atoi(e) : B2_PADROW;
   }();
   return on && g.stride == 1 && g.Ho == g.H && g.Wo == g.W && g.kh == g.kw && (g.kh & 1) && g.pad == (g.kh - 1) / 2 &&
-         c % 128 == 0 && filters <= 128 && k <= 1536 && g.W < 4096 && wpl64(filters) <= 32 &&
+         c % 128 == 0 && filters <= 256 && (filters <= 128 ? k <= 1536 : k <= 1280) && g.W < 4096 &&
          (int64_t)g.kh * g.kw * (c / 64) <= 128 &&
          // enough tiles to fill the GPU (small batches keep the one-launch path)
          (int64_t)(g.H + 1) * (g.W + 1) * batch >= (int64_t)BM * num_sms();
@@ -444,13 +444,15 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   // band rows x planes must fit a slot, and the producers' 2 x 256 units cover it
   if ((int64_t)p.R8 * 16 * p.P > PR_BAND_MAX || (int64_t)p.R8 * (p.P / 4) > 2 * 32 * PR_NPW || batch > INT32_MAX)
     return B2_EINVAL;
+  const bool wide = filters > 128;  // one 256-column tile
   CUtensorMap map;
-  if (int rc = make_bmap(&map, w_f4, filters, kpad_f4(k) / 2, 128)) return rc;
-  const int smem = padrow_smem_bytes(p.nkb);
+  if (int rc = make_bmap(&map, w_f4, filters, kpad_f4(k) / 2, wide ? 256 : 128)) return rc;
+  const int smem = wide ? padrow_smem_bytes<256>(p.nkb) : padrow_smem_bytes<128>(p.nkb);
   const bool k33 = g.kh == 3 && p.kmmas == 2;  // 3x3, c = 128: the unrolled issue loop
-  auto kern = k33 ? k_padrow_conv<3, 2> : k_padrow_conv<0, 0>;
-  static std::atomic<uint64_t> attr33{0}, attr0{0};
-  smem_optin(kern, smem, k33 ? attr33 : attr0);
+  auto kern = wide ? (k33 ? k_padrow_conv<3, 2, 256> : k_padrow_conv<0, 0, 256>)
+                   : (k33 ? k_padrow_conv<3, 2, 128> : k_padrow_conv<0, 0, 128>);
+  static std::atomic<uint64_t> attr[4];
+  smem_optin(kern, smem, attr[(wide ? 2 : 0) + (k33 ? 1 : 0)]);
   const int64_t tiles = (p.Vtotal + BM - 1) / BM;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
   void* scratch = nullptr;
@@ -473,7 +475,7 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   } else {
     p.out_bits = reinterpret_cast<uint32_t*>(out);
   }
-  launch_k(kern, grid, 32 * (4 + PR_NPW + PR_NEPI), smem, st, map, p);
+  launch_k(kern, grid, 32 * (4 + PR_NPW + (wide ? pr_nepi<256>() : pr_nepi<128>())), smem, st, map, p);
   int rc = launched();
   if (pool) {
     if (!rc) {

@@ -83,10 +83,30 @@ constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot
 // thread's 18 descriptor offsets for 3x3 / c = 128 stay in registers and the
 // MMA loop is fully unrolled: a runtime loop reading them from shared memory
 // issued one MMA per ~113 cycles, slower than the 64-cycle MMA itself)
-template <int KH, int KMMAS>
-__global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
+// BNT = 128: three 128-column accumulators, PR_NEPI epilogue warps, four
+// band slots; BNT = 256 (up to 256 filters, weights <= 160 KB): one
+// 256-column accumulator (2 x 256 + the scale columns exceed TMEM), eight
+// epilogue warps, three band slots.
+template <int BNT>
+constexpr int pr_nepi() {
+  return BNT == 256 ? 8 : PR_NEPI;
+}
+template <int BNT>
+constexpr int pr_acc() {
+  return BNT == 256 ? 1 : PR_ACC;
+}
+template <int BNT>
+constexpr int pr_bands() {
+  return BNT == 256 ? 3 : PR_BANDS;
+}
+
+template <int KH, int KMMAS, int BNT>
+__global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
     k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
-  constexpr int BN = 128;
+  constexpr int BN = BNT;
+  constexpr int PR_NEPI = pr_nepi<BNT>();
+  constexpr int PR_ACC = pr_acc<BNT>();
+  constexpr int PR_BANDS = pr_bands<BNT>();
   constexpr uint32_t IDESC = idesc_f4(BN);
   constexpr int EPI0 = 4 + PR_NPW;
   constexpr int ACC_COLS = BN;
@@ -284,7 +304,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const int et = (warp - EPI0) * 32 + lane;
-    constexpr int ECH = 4 / (PR_NEPI / 4);        // 32-column chunks per epilogue warp
+    constexpr int ECH = (BN / 32) / (PR_NEPI / 4);  // 32-column chunks per epilogue warp
     const int c0 = ((warp - EPI0) >> 2) * ECH;    // first chunk of this warp
     {
       Args ga{};
@@ -343,9 +363,10 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + PR_NEPI), 1)
   }
 }
 
+template <int BNT>
 inline int padrow_smem_bytes(int nkb) {
-  return nkb * 128 * 128 + PR_BANDS * PR_BAND_MAX + 64 * 16 + 16 + 8 * (1 + 2 * PR_BANDS + 2 * PR_ACC) + 16 +
-         8 * 128 + 1024;  // + MMA offset table (kh*kw*kmmas <= 128)
+  return nkb * BNT * 128 + pr_bands<BNT>() * PR_BAND_MAX + BNT / 2 * 16 + BNT / 8 +
+         8 * (1 + 2 * pr_bands<BNT>() + 2 * pr_acc<BNT>()) + 16 + 8 * 128 + 1024;  // + MMA offset table (<= 128)
 }
 
 // 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for
