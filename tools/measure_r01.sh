@@ -12,7 +12,7 @@ for w in bcnn bmlp; do
   b=8192; [ $w = bmlp ] && b=16384
   timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/m_traffic_$w.csv python tools/profile_stage.py --workload $w --batch $b --map gpurun_out/m_stage_map_$w.json > /dev/null 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_padrow_conv -s 1 -c 1 -o gpurun_out/m_conv2_full -f python tools/profile_stage.py --stage 1 --reps 1 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_padrow_conv -s 2 -c 1 -o gpurun_out/m_conv2_full -f python tools/profile_stage.py --stage 1 --reps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm -s 8 -c 1 -o gpurun_out/m_conv4_full -f python tools/profile_stage.py --stage 3 --reps 1 > /dev/null 2>&1
 timeout 900 python tools/sweep.py > gpurun_out/m_sweeps.jsonl 2> gpurun_out/m_sweeps.err
 (cd tools/microbench && nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o mxf4_rate mxf4_rate.cu) && timeout 120 ./tools/microbench/mxf4_rate > gpurun_out/m_mxf4_rate.jsonl 2>&1
