@@ -28,6 +28,9 @@
 #ifndef B2_BYTES_BN128  // Input8 (u8 rows) on 128-column tiles
 #define B2_BYTES_BN128 0
 #endif
+#ifndef B2_NEPI_F4_256  // epilogue warps of fp4 256-column tiles (one accumulator: the drain stalls the MMA)
+#define B2_NEPI_F4_256 8
+#endif
 #ifndef B2_NEPI_F4_128  // epilogue warps of fp4 128-column dense tiles (MMAs twice as fast: drain faster)
 #define B2_NEPI_F4_128 8
 #endif
@@ -320,7 +323,7 @@ int launch_f4(Args g, const int8_t* b, int64_t kpad, cudaStream_t st, int64_t k)
         const int64_t tiles256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
         if (B2_SMALLM_TILES && tiles256 < B2_SMALLM_TILES)
           return launch_bn<128, AM, EM, 8, 512, 4, false, true>(g, b, kpad, k, st);
-        return launch_bn<256, AM, EM, 8, 256, 8, false, true>(g, b, kpad, k, st);
+        return launch_bn<256, AM, EM, 8, 256, B2_NEPI_F4_256, false, true>(g, b, kpad, k, st);
       }
       if constexpr (AM == A_ROWS) return launch_bn<128, AM, EM, 8, 512, B2_NEPI_F4_128, false, true>(g, b, kpad, k, st);
       return launch_bn<128, AM, EM, 8, 512, 4, false, true>(g, b, kpad, k, st);

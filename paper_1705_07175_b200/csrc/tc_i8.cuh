@@ -37,6 +37,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cstdio>
+
 #include "common.cuh"
 
 namespace b2 {
@@ -871,14 +873,29 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       int acc = 0;
       uint32_t aph = 0;
       if (resb) mbar_wait(bres, 0);
+#ifdef B2_TC_TIMING
+      long long c_acc = 0, c_full = 0, c_t0 = clock64(), c_x;
+#endif
       for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+#ifdef B2_TC_TIMING
+        c_x = clock64();
+#endif
         mbar_wait(&tempty[acc], aph ^ 1);
+#ifdef B2_TC_TIMING
+        c_acc += clock64() - c_x;
+#endif
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
         int kb0, kb1;
         item_krange(g, ksp, t, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef B2_TC_TIMING
+          c_x = clock64();
+#endif
           mbar_wait(&full[s], ph);
+#ifdef B2_TC_TIMING
+          c_full += clock64() - c_x;
+#endif
           tc_fence_after();
           const uint32_t bs = smem_u32(sb + (resb ? kb : s) * B_STAGE_BYTES);
           const int kmma = kb + 1 == g.nkb ? g.klast : BKS / KMMA;
@@ -905,6 +922,11 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         tc_commit(&tfull[acc]);
         if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
       }
+#ifdef B2_TC_TIMING
+      if (blockIdx.x < 2)
+        printf("AM %d BN %d: total %lld  wait acc %lld  wait full %lld  items %lld\n", AM, BN, clock64() - c_t0, c_acc,
+               c_full, (items - blockIdx.x + gridDim.x - 1) / gridDim.x);
+#endif
     }
   } else if (warp >= 4 && warp < EPI0) {
     // ------------------------------------------------ A producers
