@@ -284,6 +284,20 @@ int b2_tc4_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int 
                              const int8_t* w_f4, int64_t filters, int kh, int kw, int stride, int pad, int pool,
                              b2_thresh th_out, void* scratch, uint64_t* out, void* stream);
 
+/* Byte-BN first layer on the padded-row fp4 kernel (_PackedByteBN ->
+ * _PackedConv [-> _Pool 2x2/2] -> _PackedBN, as b2_byte_conv_bn_pack):
+ * stride 1, odd kh == kw, pad = (kh - 1) / 2, c <= 8, filters <= 128.  The
+ * image is thresholded per channel while the band is built (no unrolled
+ * scratch); each window cell is one K=64 MMA.  Weights in the per-cell
+ * layout of b2_expand_f4_cells: rows of b2_f4_cells_row_bytes(kh * kw)
+ * bytes (per cell 64 e2m1 elements, the cell's c channel bits then zeros).
+ * Pooled calls take a stream-ordered scratch like b2_tc4_conv_bn_pack. */
+int64_t b2_f4_cells_row_bytes(int cells);
+int b2_expand_f4_cells(const uint64_t* w, int64_t rows, int64_t wpl, int cells, int c, uint8_t* out, void* stream);
+int b2_tc4_byte_conv_padrow(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
+                            const uint8_t* w_cells, int64_t filters, int kh, int kw, int pad, int pool,
+                            b2_thresh th_out, uint64_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

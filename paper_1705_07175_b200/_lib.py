@@ -73,6 +73,10 @@ SIGNATURES = {
                                        Thresh, vp, vp, vp]),
     "b2_f4_kpad": (i64, [i64]),
     "b2_expand_f4": (cint, [vp, i64, i64, i64, vp, vp]),
+    "b2_f4_cells_row_bytes": (i64, [cint]),
+    "b2_expand_f4_cells": (cint, [vp, i64, i64, cint, cint, vp, vp]),
+    "b2_tc4_byte_conv_padrow": (cint, [vp, i64, cint, cint, cint, Thresh, vp, i64, cint, cint, cint, cint, Thresh, vp,
+                                       vp]),
 }
 # fp4-weight twins of the tensor-core entry points (same arguments)
 for _n in ("bgemm", "dense_bn_pack", "dense_affine_f64", "conv_forward", "conv_bn_pack", "byte_conv_bn_pack"):

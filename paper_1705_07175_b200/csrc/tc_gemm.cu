@@ -420,42 +420,51 @@ inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t 
          (int64_t)(g.H + 1) * (g.W + 1) * batch >= (int64_t)BM * num_sms();
 }
 
-inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c, const int8_t* w_f4, int64_t filters,
-                         int64_t k, int pool, uint64_t* out, cudaStream_t st) {
-  PadArgs p{};
-  p.x = reinterpret_cast<const uint32_t*>(lines);
+// Shared padded-row geometry (virtual grid W + pad wide, H + pad tall per image).
+inline void padrow_geometry(PadArgs& p, int64_t batch, int h, int w, int kh, int kw, int pad) {
   p.N = (int)batch;
-  p.H = g.H;
-  p.W = g.W;
-  p.sstride = g.sstride;
-  p.P = c / 32;
-  p.kh = g.kh;
-  p.kw = g.kw;
-  p.pad = g.pad;
-  p.Wp = g.W + 1;
-  p.VI = (int64_t)(g.H + 1) * p.Wp;
+  p.H = h;
+  p.W = w;
+  p.kh = kh;
+  p.kw = kw;
+  p.pad = pad;
+  // pad zero columns per row and pad zero rows per image: a window reaching
+  // pad cells past any edge lands on zeros
+  p.Wp = w + (pad > 0 ? pad : 1);
+  p.VI = (int64_t)(h + (pad > 0 ? pad : 1)) * p.Wp;
   p.Vtotal = p.VI * batch;
   p.vi_magic = ~0ull / (uint64_t)p.VI + 1;  // ceil(2^64 / VI), exact multiply-high division for v < 2^40
   p.wp_magic = (uint32_t)((((uint64_t)1 << 32) + p.Wp - 1) / p.Wp);
-  p.R8 = ((2 * p.Wp + 2 + BM) + 7) / 8 * 8;
-  p.nkb = (int)((k + 255) / 256);
-  p.F = (int)filters;
-  p.kmmas = p.P / 2;
-  p.ldo32 = 2 * wpl64(filters);
-  p.thresh = g.thresh;
-  p.ge = g.ge;
-  // band rows x planes must fit a slot, and the producers' 2 x 256 units cover it
-  if ((int64_t)p.R8 * 16 * p.P > PR_BAND_MAX || (int64_t)p.R8 * (p.P / 4) > 2 * 32 * PR_NPW || batch > INT32_MAX)
+  p.band0 = pad * p.Wp + pad;  // the window's reach above (and below) a virtual row
+  p.R8 = ((2 * p.band0 + BM) + 7) / 8 * 8;
+}
+
+// Launch the padded-row kernel (and, pooled, the bit-pool pass on a
+// stream-ordered scratch).  p.nkb, p.P, p.kmmas, p.F, p.thresh/ge set by the caller.
+template <bool BYTEIN>
+inline int padrow_run(PadArgs& p, const int8_t* w, int64_t b_row_bytes, int pool, uint64_t* out, cudaStream_t st) {
+  if ((int64_t)p.R8 * 16 * p.P > PR_BAND_MAX || (int64_t)p.R8 * (BYTEIN ? 1 : p.P / 4) > 2 * 32 * PR_NPW ||
+      p.N < 0)
     return B2_EINVAL;
-  const bool wide = filters > 128;  // one 256-column tile
+  p.ldo32 = 2 * wpl64(p.F);
+  const bool wide = p.F > 128;  // one 256-column tile
+  if (BYTEIN && wide) return B2_EINVAL;
   CUtensorMap map;
-  if (int rc = make_bmap(&map, w_f4, filters, kpad_f4(k) / 2, wide ? 256 : 128)) return rc;
+  if (int rc = make_bmap(&map, w, p.F, b_row_bytes, wide ? 256 : 128)) return rc;
   const int smem = wide ? padrow_smem_bytes<256>(p.nkb) : padrow_smem_bytes<128>(p.nkb);
-  const bool k33 = g.kh == 3 && p.kmmas == 2;  // 3x3, c = 128: the unrolled issue loop
-  auto kern = wide ? (k33 ? k_padrow_conv<3, 2, 256> : k_padrow_conv<0, 0, 256>)
-                   : (k33 ? k_padrow_conv<3, 2, 128> : k_padrow_conv<0, 0, 128>);
+  static const bool generic_only = getenv("B2_PR_GENERIC") && atoi(getenv("B2_PR_GENERIC"));  // test hook
+  const bool k3 = !generic_only && p.kh == 3 && p.kmmas == (BYTEIN ? 1 : 2);  // the unrolled 3x3 issue loops
+  void (*kern)(CUtensorMap, PadArgs);
+  if constexpr (BYTEIN)
+    kern = k3 ? k_padrow_conv<3, 1, 128, true> : k_padrow_conv<0, 0, 128, true>;
+  else
+    kern = wide ? (k3 ? k_padrow_conv<3, 2, 256> : k_padrow_conv<0, 0, 256>)
+                : (k3 ? k_padrow_conv<3, 2, 128> : k_padrow_conv<0, 0, 128>);
+  // the size depends on the layer (weight atoms): opt in to the whole 227 KB
+  // once per kernel and device, so any later, larger layer fits too
   static std::atomic<uint64_t> attr[4];
-  smem_optin(kern, smem, attr[(wide ? 2 : 0) + (k33 ? 1 : 0)]);
+  if (smem > 227 * 1024) return B2_EINVAL;
+  smem_optin(kern, 227 * 1024, attr[(wide ? 2 : 0) + (k3 ? 1 : 0)]);
   const int64_t tiles = (p.Vtotal + BM - 1) / BM;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
   void* scratch = nullptr;
@@ -473,7 +482,7 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
       }
       pool_kept.fetch_or(1ull << (dev & 63));
     }
-    if (cudaMallocAsync(&scratch, (size_t)batch * g.H * g.W * p.ldo32 * 4, st) != cudaSuccess) return launched();
+    if (cudaMallocAsync(&scratch, (size_t)p.N * p.H * p.W * p.ldo32 * 4, st) != cudaSuccess) return launched();
     p.out_bits = reinterpret_cast<uint32_t*>(scratch);
   } else {
     p.out_bits = reinterpret_cast<uint32_t*>(out);
@@ -482,14 +491,30 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   int rc = launched();
   if (pool) {
     if (!rc) {
-      const int64_t n = batch * (g.H / 2) * (g.W / 2);  // pooled sites
-      launch_k(k_pool_bits, (unsigned)cdiv(n, 256), 256, 0, st, (const uint32_t*)scratch, batch, g.H, g.W, p.ldo32,
-               g.ge, (int)filters, reinterpret_cast<uint32_t*>(out));
+      const int64_t n = (int64_t)p.N * (p.H / 2) * (p.W / 2);  // pooled sites
+      launch_k(k_pool_bits, (unsigned)cdiv(n, 256), 256, 0, st, (const uint32_t*)scratch, (int64_t)p.N, p.H, p.W,
+               p.ldo32, p.ge, p.F, reinterpret_cast<uint32_t*>(out));
       rc = launched();
     }
     cudaFreeAsync(scratch, st);
   }
   return rc;
+}
+
+inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c, const int8_t* w_f4, int64_t filters,
+                         int64_t k, int pool, uint64_t* out, cudaStream_t st) {
+  if (batch > INT32_MAX) return B2_EINVAL;
+  PadArgs p{};
+  padrow_geometry(p, batch, g.H, g.W, g.kh, g.kw, g.pad);
+  p.x = reinterpret_cast<const uint32_t*>(lines);
+  p.sstride = g.sstride;
+  p.P = c / 32;
+  p.nkb = (int)((k + 255) / 256);
+  p.F = (int)filters;
+  p.kmmas = p.P / 2;
+  p.thresh = g.thresh;
+  p.ge = g.ge;
+  return padrow_run<false>(p, w_f4, kpad_f4(k) / 2, pool, out, st);
 }
 
 inline void pack_args(Args& g, const b2_thresh& th, uint64_t* out, int64_t n) {
@@ -636,6 +661,42 @@ int b2_expand_i8(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, int pe
 }
 
 int64_t b2_f4_kpad(int64_t k) { return tc::kpad_f4(k); }
+
+int64_t b2_f4_cells_row_bytes(int cells) { return cells < 1 ? -1 : tc::kpad_f4((int64_t)cells * 64) / 2; }
+
+int b2_expand_f4_cells(const uint64_t* w, int64_t rows, int64_t wpl, int cells, int c, uint8_t* out, void* stream) {
+  if (rows < 0 || cells < 1 || c < 1 || c > 8 || (int64_t)cells * c > 64 * wpl) return B2_EINVAL;
+  const int64_t row_words = tc::kpad_f4((int64_t)cells * 64) / 8;
+  const int64_t n = rows * row_words;
+  if (!n) return 0;
+  launch_k(tc::k_expand_f4_cells, (unsigned)cdiv(n, 256), 256, 0, S(stream), w, rows, wpl, cells, c, row_words,
+           reinterpret_cast<uint32_t*>(out));
+  return launched();
+}
+
+int b2_tc4_byte_conv_padrow(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
+                            const uint8_t* w_cells, int64_t filters, int kh, int kw, int pad, int pool,
+                            b2_thresh th_out, uint64_t* out, void* stream) {
+  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, 1, pad) || c > 8 || filters > 128 || kh != kw || !(kh & 1) ||
+      pad != (kh - 1) / 2 || kh * kw > 128 || !th_in.thresh || !th_in.ge_dir || !th_out.thresh || !th_out.ge_dir ||
+      (pool && ((h & 1) || (w & 1))) || batch > INT32_MAX || w >= 4096)
+    return B2_EINVAL;
+  if (!batch) return 0;
+  tc::PadArgs p{};
+  tc::padrow_geometry(p, batch, h, w, kh, kw, pad);
+  p.xb = x;
+  p.cin = c;
+  p.th_in = th_in.thresh;
+  p.ge_in = th_in.ge_dir;
+  p.P = 2;  // data plane + zero plane: one K=64 MMA per window cell
+  p.kmmas = 1;
+  p.nkb = (int)((kh * kw * 64 + 255) / 256);
+  p.F = (int)filters;
+  p.thresh = th_out.thresh;
+  p.ge = th_out.ge_dir;
+  return tc::padrow_run<true>(p, reinterpret_cast<const int8_t*>(w_cells), b2_f4_cells_row_bytes(kh * kw), pool, out,
+                              S(stream));
+}
 
 int b2_expand_f4(const uint64_t* w, int64_t rows, int64_t wpl, int64_t k, uint8_t* out, void* stream) {
   if (rows < 0 || wpl < 1 || k < 1 || k > 64 * wpl) return B2_EINVAL;

@@ -34,11 +34,12 @@ struct PadArgs {
   const uint32_t* x;   // NHWC-bits input, sstride words per pixel
   int N, H, W, sstride, P;  // P = c / 32 words (= K planes) per pixel
   int kh, kw, pad;
-  int Wp;              // W + 1
+  int Wp;              // W + pad (pad zero columns per virtual row)
   int64_t VI, Vtotal;  // virtual rows per image, in all
   uint64_t vi_magic;   // ceil(2^64 / VI): image of a virtual row by one multiply-high
   uint32_t wp_magic;   // ceil(2^32 / Wp): row within the image
-  int R8;              // band rows (multiple of 8)
+  int R8;              // band rows (multiple of 8): 128 + 2 * band0
+  int band0;           // halo above a tile: pad * Wp + pad virtual rows
   int nkb;             // 128-byte B atoms (256 K elements) in shared memory
   int F;               // filters (<= 128)
   int kmmas;           // K=64 MMAs per window cell (= P / 2)
@@ -46,6 +47,12 @@ struct PadArgs {
   int64_t ldo32;
   const int32_t* thresh;
   const uint8_t* ge;
+  // BYTEIN (byte-BN first layer): u8 image (N, H, W, cin), per-channel
+  // byte thresholds; one data plane per pixel (cin <= 8 bits) + a zero plane
+  const uint8_t* xb;
+  int cin;
+  const int32_t* th_in;
+  const uint8_t* ge_in;
 };
 
 #ifndef B2_PADROW_LBO_K
@@ -100,7 +107,7 @@ constexpr int pr_bands() {
   return BNT == 256 ? 3 : PR_BANDS;
 }
 
-template <int KH, int KMMAS, int BNT>
+template <int KH, int KMMAS, int BNT, bool BYTEIN = false>
 __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
     k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
   constexpr int BN = BNT;
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
       int nmma = 0;
       for (int cy = 0; cy < g.kh; ++cy)
         for (int cx = 0; cx < g.kw; ++cx) {
-          const int off = (g.Wp + 1) + (cy - g.pad) * g.Wp + (cx - g.pad);  // band row of tile row 0
+          const int off = g.band0 + (cy - g.pad) * g.Wp + (cx - g.pad);  // band row of tile row 0
           const int cell = cy * g.kw + cx;
           for (int kc = 0; kc < g.kmmas; ++kc, ++nmma) {
             const int k = cell * g.P * 32 + kc * 64;  // K element
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
               for (int kc = 0; kc < KMMAS; ++kc) {
                 const int cell = cy * KH + cx;
                 const int k = (cell * KMMAS + kc) * 64;  // K element (c = 32 * 2 * KMMAS)
-                const uint32_t off = (uint32_t)((g.Wp + 1) + (cy - PAD) * g.Wp + (cx - PAD));
+                const uint32_t off = (uint32_t)(g.band0 + (cy - PAD) * g.Wp + (cx - PAD));
                 const uint32_t ao = ((uint32_t)(2 * kc) * plane_bytes + off * 16u) >> 4;
                 const uint32_t bo = (uint32_t)((k >> 8) * BN * 128 + ((k & 255) >> 6) * 32) >> 4;
                 tc_mma_f4(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
@@ -245,6 +252,61 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
     }
   } else if (warp >= 4 && warp < EPI0) {
     // ------------------------------------------------ band producers
+    if constexpr (BYTEIN) {
+      // byte-BN first layer: one band row per thread per tile; plane 0 =
+      // the pixel's thresholded channel bits (<= 8) as e2m1, plane 1 = 0
+      const int pt = (warp - 4) * 32 + lane;  // 0 .. 255
+      int32_t tin[8];
+      bool gin[8];
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        tin[ch] = ch < g.cin ? __ldg(g.th_in + ch) : 0;
+        gin[ch] = ch < g.cin ? __ldg(g.ge_in + ch) != 0 : true;
+      }
+      const uint32_t cmask = (1u << g.cin) - 1u;
+      for (int sl = 0; sl < PR_BANDS; ++sl)  // the zero planes, once
+        for (int b = pt; b < g.R8; b += 32 * PR_NPW)
+          *reinterpret_cast<uint4*>(sband + sl * PR_BAND_MAX + plane_bytes + (size_t)b * 16) = make_uint4(0, 0, 0, 0);
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t v0 = t * BM - g.band0;
+        uint32_t bits[2] = {0, 0};
+        bool ok[2] = {false, false};
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int b = pt + i * 32 * PR_NPW;
+          const int64_t v = v0 + b;
+          if (b < g.R8 && v >= 0 && v < g.Vtotal) {
+            int64_t n;
+            int y, x;
+            vsplit(g, v, n, y, x);
+            if (y < g.H && x < g.W) {
+              ok[i] = true;
+              const uint8_t* px = g.xb + ((n * g.H + y) * g.W + x) * g.cin;
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch)
+                if (ch < g.cin) bits[i] |= (thr_bit((int32_t)__ldg(px + ch), tin[ch], gin[ch]) ? 1u : 0u) << ch;
+            }
+          }
+        }
+        mbar_wait_suspend(&bempty[slot], ph ^ 1);
+        uint8_t* band = sband + slot * PR_BAND_MAX;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int b = pt + i * 32 * PR_NPW;
+          if (b < g.R8) {
+            uint32_t o[4];
+            widen_f4m(bits[i], ok[i] ? cmask : 0u, o);
+            *reinterpret_cast<uint4*>(band + (size_t)b * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bfull[slot]);
+        if (++slot == PR_BANDS) slot = 0, ph ^= 1;
+      }
+    } else {
     // each thread owns up to UMAX (band row, 4-word group) units per tile;
     // a tile's loads are issued before waiting for its band slot
     constexpr int UMAX = 2;
@@ -254,7 +316,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
     int slot = 0;
     uint32_t ph = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int64_t v0 = t * BM - (g.Wp + 1);
+      const int64_t v0 = t * BM - g.band0;
       uint4 w[UMAX];
       bool ok[UMAX];
 #pragma unroll
@@ -298,6 +360,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bfull[slot]);
       if (++slot == PR_BANDS) slot = 0, ph ^= 1;
+    }
     }
   } else if (warp >= EPI0) {
     // ------------------------------------------------ epilogue
@@ -361,6 +424,31 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+}
+
+// Byte-input first-layer weights for the padded-row kernel: per window cell
+// 64 K elements — the cell's c (<= 8) channel bits as e2m1 in the first 32
+// (widen_f4 order), then 32 zeros — so each cell is one K=64 MMA reading
+// the band's data plane and zero plane.  Packed rows hold K = cells * c
+// bits in (dy, dx, c) order (the reference's layout).
+__global__ void k_expand_f4_cells(const uint64_t* __restrict__ w, int64_t rows, int64_t wpl, int cells, int c,
+                                  int64_t row_words, uint32_t* __restrict__ out) {
+  pdl_entry();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * row_words) return;
+  const int64_t r = t / row_words;
+  const int o = (int)(t - r * row_words);
+  const int cell = o >> 3, q = o & 7;
+  uint32_t word = 0;
+  if (cell < cells && q < 4) {
+    const int64_t k0 = (int64_t)cell * c;  // first bit of the cell
+    const uint64_t* line = w + r * wpl;
+    uint32_t bits = (uint32_t)(line[k0 >> 6] >> (k0 & 63));
+    if ((k0 & 63) + c > 64) bits |= (uint32_t)(line[(k0 >> 6) + 1] << (64 - (k0 & 63)));
+    const uint32_t valid = (1u << c) - 1u;
+    word = (0xAAAAAAAAu ^ ((bits << (3 - q)) & 0x88888888u)) & (((valid >> q) & 0x11111111u) * 0xFu);
+  }
+  out[t] = word;
 }
 
 template <int BNT>

@@ -195,6 +195,44 @@ def test_tc_byte_conv_bn_pack_vs_oracle(oracle, h, w, c, f, kh, pad, stride, poo
     assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
 
 
+@pytest.mark.parametrize("h,w,c,f,kh,pool,batch", [(32, 32, 3, 128, 3, False, 3), (16, 12, 3, 64, 3, True, 2),
+                                                  (8, 8, 8, 32, 3, True, 5), (10, 6, 5, 64, 5, True, 2),
+                                                  (5, 7, 1, 10, 3, False, 4), (32, 32, 3, 100, 3, True, 20)])
+def test_tc4_byte_conv_padrow_vs_oracle(oracle, h, w, c, f, kh, pool, batch):
+    """Byte-BN first layer on the padded-row fp4 kernel (stride 1, same
+    padding): the image is thresholded per channel while the band is built."""
+    rng = np.random.default_rng(7 * h * w + c + f)
+    pad = kh // 2
+    imgs = rng.integers(0, 256, (batch, h, w, c), dtype=np.uint8)
+    bn0 = rand_bn(rng, c, 100.0)
+    k = kh * kh * c
+    wt = oracle.pack_lines(rand_pm1(rng, f, k))
+    bn1 = rand_bn(rng, f, 8.0)
+    corr = oracle.compute_correction(wt, (h, w, c), (kh, kh), 1, pad)
+    want = []
+    for i in range(batch):
+        if c == 1:  # single-channel maps are per-row lines (tensor.py:165-173, network.py:121-124)
+            lines = oracle.threshold_sign_pack(imgs[i].reshape(h, w).astype(np.int64), np.repeat(bn0.thresh, w),
+                                               np.repeat(bn0.ge_dir, w), False)
+        else:
+            lines = oracle.threshold_sign_pack(imgs[i].reshape(h * w, c).astype(np.int64), bn0.thresh, bn0.ge_dir,
+                                               False)
+        acc = (oracle.bgemm(oracle.unroll_packed(lines, h, w, c, kh, kh, 1, pad), wt, k) + corr).reshape(h, w, f)
+        if pool:
+            acc = oracle.maxpool(acc, 2, 2, 2)
+        want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn1.thresh, bn1.ge_dir, False))
+    cal0 = layers.calibrate_device(bn0.mean, bn0.var, bn0.gamma, bn0.beta, bn0.eps, 255)
+    cal1 = layers.calibrate_device(bn1.mean, bn1.var, bn1.gamma, bn1.beta, bn1.eps, k)
+    row = int(_lib.raw("b2_f4_cells_row_bytes")(kh * kh))
+    wc = _dev.empty((f, row), np.uint8)
+    _lib.call("b2_expand_f4_cells", _dev.P(_dev.upload(wt)), f, -(-k // 64), kh * kh, c, _dev.P(wc), _dev.stream())
+    sites = h * w // (4 if pool else 1)
+    out = _dev.empty((batch, sites, -(-f // 64)), np.uint64)
+    _lib.call("b2_tc4_byte_conv_padrow", _dev.P(_dev.upload(imgs)), batch, h, w, c, th(cal0), _dev.P(wc), f, kh, kh,
+              pad, int(pool), th(cal1), _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
+
+
 @pytest.mark.parametrize("name", ["bcnn", "bmlp"])
 def test_network_engines_agree(networks_golden, name, monkeypatch):
     spec = zoo.bcnn_spec() if name == "bcnn" else zoo.bmlp_spec()
