@@ -6,8 +6,9 @@ from paper_1705_07175_b200 import zoo, forward_batch
 from paper_1705_07175_b200.network import Network
 PLANS = {"bmlp": [[2048, 4096, 10240], [1024, 2048, 4096, 9216], [4096, 12288], [2048, 14336], [1024, 15360],
                   [4096, 4096, 8192], [8192, 8192], [16384]],
-         "bcnn": [[1024, 2048, 5120], [512, 7680], [1024, 7168], [2048, 6144], [8192]]}
-for name, spec, B in (("bmlp", zoo.bmlp_spec(), 16384), ("bcnn", zoo.bcnn_spec(), 8192)):
+         "bcnn": [[1536, 6656], [1024, 7168], [768, 7424], [512, 2048, 5632], [512, 1536, 6144], [256, 1280, 6656],
+                  [1024, 3072, 4096]]}
+for name, spec, B in (("bcnn", zoo.bcnn_spec(), 8192),):
     net = Network(spec, max_batch=B)
     imgs = net.pinned_images(B); imgs[:] = 3
     out = net.pinned_scores(B)
