@@ -236,11 +236,13 @@ static int num_sms() {
 // KS: split-K over thread-block clusters of g.ksplit CTAs (one tile's K
 // splits), one work item per CTA.
 template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4), bool KS = false, bool F4 = false>
-int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st) {
+int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st, const CUtensorMap* amap = nullptr) {
   g.nkb = (int)((k + BKS - 1) / BKS);
   g.klast = (int)(((k - 1) % BKS) / (F4 ? 64 : 32) + 1);
   // one N tile whose every K stage fits the B ring space: keep it resident
-  const int b_room = F4 ? f4_stages<BN, BKS>() : b_stages<BN, BKS>();
+  const int b_room = F4                    ? f4_stages<BN, BKS>()
+                     : AM == A_BYTES_TMA ? (192 * 1024) / ((BN + BM) * BKS)
+                                         : b_stages<BN, BKS>();
   g.resb = (!KS && g.N <= BN && g.nkb <= b_room && B2_RESIDENT_B) ? 1 : 0;
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, F4 ? kpad / 2 : kpad, BN)) return rc;
@@ -249,12 +251,17 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   static std::atomic<uint64_t> attr{0};
   smem_optin(kern, smem, attr);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  CUtensorMap amap_v;  // A_BYTES_TMA: the u8 rows; unused otherwise
+  if (amap)
+    amap_v = *amap;
+  else
+    memset(&amap_v, 0, sizeof(amap_v));
   if constexpr (KS) {
-    launch_kc(g.ksplit, kern, (unsigned)(tiles * g.ksplit), num_threads<NPW, NEPI>(), smem, st, map, g);
+    launch_kc(g.ksplit, kern, (unsigned)(tiles * g.ksplit), num_threads<NPW, NEPI>(), smem, st, map, amap_v, g);
   } else {
     g.ksplit = 1;
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    launch_k(kern, grid, num_threads<NPW, NEPI>(), smem, st, map, g);
+    launch_k(kern, grid, num_threads<NPW, NEPI>(), smem, st, map, amap_v, g);
   }
   return launched();
 }
@@ -332,9 +339,13 @@ int launch_f4(Args g, const int8_t* b, int64_t kpad, cudaStream_t st, int64_t k)
 }
 
 template <int AM, int EM, bool F4 = false>
-int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k) {
+int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k, const CUtensorMap* amap = nullptr) {
   if (g.M == 0 || g.N == 0) return 0;
   if constexpr (F4) return launch_f4<AM, EM>(g, b_i8, kpad, st, k);
+  if constexpr (AM == A_BYTES_TMA) {
+    if (g.N > 128) return launch_bn<256, AM, EM, 0, 128, 8>(g, b_i8, kpad, k, st, amap);
+    return launch_bn<128, AM, EM, 0, 128, 4>(g, b_i8, kpad, k, st, amap);
+  } else {
   if (int ks = splitk_count<AM, EM>(g, k)) {
     if constexpr ((EM == E_PACK || EM == E_POOLPACK) && (AM == A_ROWS || AM == A_CONV)) {
       g.ksplit = ks;
@@ -363,6 +374,7 @@ int launch(Args g, const int8_t* b_i8, int64_t kpad, cudaStream_t st, int64_t k)
   } else {
     if (AM == A_CONV && g.spw % 4 != 0) return launch_bn<128, AM, EM, 8, 128>(g, b_i8, kpad, k, st);
     return launch_bn<128, AM, EM, B2_NPW128, B2_BKS128>(g, b_i8, kpad, k, st);
+  }
   }
 }
 
@@ -749,6 +761,24 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
   g.M = batch;
   g.N = (int)units;
   tc::pack_args(g, th, out, units);
+  // u8 rows whose pitch and base TMA can address: loaded by TMA straight into
+  // shared memory (no producer warps), int8 MMA with A from shared memory
+  static const int use_tma = [] {
+    const char* e = getenv("B2_INPUT8_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  if (use_tma && batch && k % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && batch <= INT32_MAX) {
+    auto fn = tc::encode_fn();
+    CUtensorMap amap;
+    cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)batch};
+    cuuint64_t strides[1] = {(cuuint64_t)k};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+    cuuint32_t estr[2] = {1, 1};
+    if (fn && fn(&amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(x), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      return tc::launch<tc::A_BYTES_TMA, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k, &amap);
+  }
   return tc::launch<tc::A_BYTES, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
 }
 

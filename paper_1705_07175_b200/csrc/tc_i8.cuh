@@ -51,7 +51,9 @@ constexpr int PF = 4;                   // A-producer prefetch depth (K blocks)
 
 // A operand sources: packed rows; implicit bit-im2col of NHWC-bits
 // activations; raw u8 rows; masked window rows of the byte-input first conv
-enum AMode { A_ROWS = 0, A_CONV = 1, A_BYTES = 2, A_BYTECONV = 3 };
+// A_BYTES_TMA: u8 rows loaded by TMA into shared memory (no producer warps;
+// the int8 MMA reads A from shared memory)
+enum AMode { A_ROWS = 0, A_CONV = 1, A_BYTES = 2, A_BYTECONV = 3, A_BYTES_TMA = 4 };
 enum EMode { E_I32 = 0, E_PACK = 1, E_POOLPACK = 2, E_AFFINE = 3 };
 
 struct Args {
@@ -176,6 +178,15 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint32_t a_tmem, uint
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -739,32 +750,39 @@ constexpr int num_threads() {
 // as fast).
 template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4>
 __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
+                                                                  const __grid_constant__ CUtensorMap amap,
                                                                   const Args g) {
+  constexpr bool ATMA = AM == A_BYTES_TMA;  // A by TMA into shared memory, no producer warps
+  constexpr bool ASMEM = F4 || ATMA;        // A ring in shared memory
   constexpr int WS = BKS / 32;        // K words per stage
-  constexpr int HALVES = NPW / 4;     // producer warps per lane quarter
+  constexpr int HALVES = NPW >= 4 ? NPW / 4 : 1;  // producer warps per lane quarter
   constexpr int WPH = WS / HALVES;    // K words per producer thread per stage
   constexpr int A_STAGE_COLS = BKS / 4;
   constexpr int EPI0 = 4 + NPW;       // first epilogue warp
-  static_assert(WPH == 2 || WPH == 4 || WPH == 8, "producer word split");
+  static_assert(ATMA || WPH == 2 || WPH == 4 || WPH == 8, "producer word split");
+  static_assert(!ATMA || (NPW == 0 && !F4 && !KS), "TMA-fed u8 rows: int8, no producers, no split-K");
   constexpr bool POOLED = (EM == E_POOLPACK);
   static_assert(!F4 || AM != A_BYTES, "u8 rows are not fp4 operands");
   constexpr int B_STAGE_BYTES = F4 ? BN * BKS / 2 : BN * BKS;
-  constexpr int A_STAGE_BYTES = BM * BKS / 2;  // fp4: A stage in shared memory
+  constexpr int A_STAGE_BYTES = F4 ? BM * BKS / 2 : BM * BKS;  // A stage in shared memory (fp4 / TMA-fed u8)
   constexpr int KMMA = F4 ? 64 : 32;            // K per MMA instruction
   constexpr int VW = F4 ? 4 : 8;                // widened words per 32-bit input word
   // one ring: stage s = B tile in shared memory + A block in TMEM, one
   // full barrier (TMA bytes + producer warps) and one empty barrier (MMA
   // commit): the issuing thread's per-stage waits and commits are serial
   // time the tensor pipe cannot hide at N = 128 (tools/microbench/mma_loop.cu)
-  constexpr int SA = F4 ? f4_stages<BN, BKS>()
-                       : (a_stages<BN, AM, BKS>() < b_stages<BN, BKS>() ? a_stages<BN, AM, BKS>() : b_stages<BN, BKS>());
+  constexpr int SA = F4     ? f4_stages<BN, BKS>()
+                     : ATMA ? (192 * 1024) / (B_STAGE_BYTES + A_STAGE_BYTES)
+                            : (a_stages<BN, AM, BKS>() < b_stages<BN, BKS>() ? a_stages<BN, AM, BKS>() : b_stages<BN, BKS>());
   constexpr int SB = SA;
   constexpr int ACC_COLS = BN;
-  constexpr int ACC_BUFS = F4 ? f4_acc_bufs<BN>() : acc_bufs<BN, AM>();
+  // TMA-fed u8: TMEM holds only accumulators (no scale factors for int8): double-buffered even at 256 columns
+  constexpr int ACC_BUFS = F4 ? f4_acc_bufs<BN>() : ATMA ? (BN > 128 ? 2 : 3) : acc_bufs<BN, AM>();
   constexpr int A_COL0 = ACC_BUFS * ACC_COLS;  // i8: A ring; fp4: scale-factor columns
-  static_assert(F4 ? (A_COL0 + F4_SF_COLS <= 512) : (A_COL0 + SA * A_STAGE_COLS <= 512), "TMEM budget");
-  constexpr uint32_t IDESC = F4 ? idesc_f4(BN) : idesc_i8(BN, AM == A_BYTES);
-  constexpr int B_REGION = F4 ? SB * B_STAGE_BYTES : b_stages<BN, BKS>() * B_STAGE_BYTES;
+  static_assert(F4 ? (A_COL0 + F4_SF_COLS <= 512) : ATMA ? (A_COL0 <= 512) : (A_COL0 + SA * A_STAGE_COLS <= 512),
+                "TMEM budget");
+  constexpr uint32_t IDESC = F4 ? idesc_f4(BN) : idesc_i8(BN, AM == A_BYTES || ATMA);
+  constexpr int B_REGION = ASMEM ? SB * B_STAGE_BYTES : b_stages<BN, BKS>() * B_STAGE_BYTES;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the shared array (an
@@ -774,7 +792,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   // the B region is sized for b_stages() (a resident B tile may use all of it);
   // fp4: the A ring follows it
   uint8_t* sa = smem + B_REGION;
-  int4* sthr = reinterpret_cast<int4*>(smem + B_REGION + (F4 ? SA * A_STAGE_BYTES : 0));  // THR_COLS/2 x (mul, add, ...)
+  int4* sthr = reinterpret_cast<int4*>(smem + B_REGION + (ASMEM ? SA * A_STAGE_BYTES : 0));  // THR_COLS/2 x (mul, add, ...)
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + THR_COLS / 2);        // THR_COLS/32 ge-direction masks
   uint64_t* full = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
   uint64_t* empty = full + SA;
@@ -795,7 +813,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&full[s], NPW + (resb ? 0 : 1));  // every A-producer warp (+ the TMA expect_tx arrival)
+      // every A-producer warp (+ the TMA expect_tx arrival; TMA-fed A: that arrival only)
+      mbar_init(&full[s], ATMA ? 1 : NPW + (resb ? 0 : 1));
       mbar_init(&empty[s], 1);
     }
     mbar_init(bres, 1);
@@ -805,6 +824,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
+    if constexpr (ATMA) asm volatile("prefetch.tensormap [%0];" ::"l"(&amap) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -851,12 +871,24 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         const int n0 = (int)(t / ksp / mtiles) * BN;
         if constexpr ((AM == A_CONV || AM == A_ROWS) && !KS)
           prefetch_tile_inputs<AM>(g, t + 2 * (int64_t)gridDim.x, mtiles, tiles);
-        if (resb) continue;
+        if (resb && !ATMA) continue;
         int kb0, kb1;
         item_krange(g, ksp, t, kb0, kb1);
+        const int m0 = (int)((t % mtiles) * BM);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_nc(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], B_STAGE_BYTES);
+          if constexpr (ATMA) {  // this stage's A boxes (u8 rows m0.., K bytes kb*BKS..), then B unless resident
+            mbar_expect_tx(&full[s], A_STAGE_BYTES + (resb ? 0 : B_STAGE_BYTES));
+#pragma unroll
+            for (int at = 0; at < BKS / BK; ++at)
+              tma_load_2d(sa + s * A_STAGE_BYTES + at * BM * BK, &amap, &full[s], kb * BKS + at * BK, m0);
+            if (resb) {
+              if (++s == SB) s = 0, ph ^= 1;
+              continue;
+            }
+          } else {
+            mbar_expect_tx(&full[s], B_STAGE_BYTES);
+          }
 #pragma unroll
           for (int at = 0; at < (F4 ? BKS / 256 : BKS / BK); ++at)  // one 128-byte-wide box per swizzle atom
             tma_load_2d(sb + s * B_STAGE_BYTES + at * BN * BK, &bmap, &full[s], (F4 ? kb * BKS / 2 : kb * BKS) + at * BK,
@@ -908,6 +940,14 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
                 tc_mma_f4(d, sw128_desc(as + (k >> 2) * BM * BK + (k & 3) * 32),
                           sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, tmem + A_COL0,
                           tmem + A_COL0 + 4, (kb > kb0 || k) ? 1u : 0u);
+          } else if constexpr (ATMA) {
+            // u8 A and s8 B both in shared memory (128-byte swizzle, K-major)
+            const uint32_t as = smem_u32(sa + s * A_STAGE_BYTES);
+#pragma unroll
+            for (int k = 0; k < BKS / 32; ++k)
+              if (k < kmma)
+                tc_mma_i8_ss(d, sw128_desc(as + (k >> 2) * BM * BK + (k & 3) * 32),
+                             sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, (kb > kb0 || k) ? 1u : 0u);
           } else {
             const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
 #pragma unroll
@@ -1346,7 +1386,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 
 template <int BN, int AM, int BKS, bool F4 = false>
 constexpr int smem_bytes() {
-  if constexpr (F4)
+  if constexpr (AM == A_BYTES_TMA)
+    return (192 * 1024) / ((BN + BM) * BKS) * (BN + BM) * BKS + THR_COLS * 8 + THR_COLS / 8 + 8 * (2 * 8 + 11) + 16 +
+           1024;
+  else if constexpr (F4)
     return f4_stages<BN, BKS>() * (BN + BM) * BKS / 2 + THR_COLS * 8 + THR_COLS / 8 +
            8 * (2 * f4_stages<BN, BKS>() + 7) + 16 + 1024;
   else
