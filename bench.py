@@ -364,6 +364,7 @@ def run_ours(args, rank, world, local_rank):
     stage_total = sum(s["ms"] for s in stages)
     batch1 = batch1_latency(spec, shape) if rank == 0 else None
     others = other_metrics(args, dev, flush) if rank == 0 and not args.no_extra else None
+    sweep = batch_sweep(flush) if rank == 0 and not args.no_extra else None
     int8_peak, int8_src = measure_int8_peak(dev)
     fp4_peak, fp4_src = measure_fp4_peak(dev)
     peaks = {"f4": (fp4_peak, fp4_src), "i8": (int8_peak, int8_src), "popc": (POPC_PEAK_TBITOPS, POPC_PEAK_SOURCE)}
@@ -396,6 +397,7 @@ def run_ours(args, rank, world, local_rank):
         "stages": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in s_.items()} for s_ in stages],
         "batch1": batch1,
         "other_metrics": others,
+        "batch_sweep": sweep,
     }
     return result
 
@@ -448,6 +450,38 @@ def other_metrics(args, dev, flush, steps: int = 10):
     out["bgemm_8192_Gops"] = 2.0 * n ** 3 * 5 / (ms / 1e3) / 1e9
     out["bgemm_operand_format"] = _lib.TC_FORMAT
     out["note"] = "device time, CUDA events, L2 flushed between steps; ops = 2 per binary MAC"
+    return out
+
+
+def batch_sweep(flush, reps: int = 20):
+    """BASELINE configs[0] / configs[1] batch sizes (BMLP 1 and 256, BCNN 1,
+    128 and 1024): device throughput of one CUDA-graph replay of the whole
+    network per step on resident input, CUDA events, L2 flushed between
+    steps.  Batch 1 here is device time; `batch1` below is the wall-clock
+    latency of the public `forward` call."""
+    import torch
+    from paper_1705_07175_b200.network import Network
+    out = {}
+    for name, batches in (("bmlp", (1, 256)), ("bcnn", (1, 128, 1024))):
+        spec, shape = build_workload(name)
+        for b in batches:
+            net = Network(spec, max_batch=b)
+            x = np.random.default_rng(b).integers(0, 256, (b, int(np.prod(shape))), dtype=np.uint8)
+            net.input_device[:b].copy_(torch.from_numpy(x).cuda())
+            for _ in range(3):
+                net.run(b)
+            torch.cuda.synchronize()
+            ms = 0.0
+            for _ in range(reps):
+                flush.fill_(3)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                net.run(b)
+                e1.record()
+                torch.cuda.synchronize()
+                ms += e0.elapsed_time(e1)
+            out[f"{name}_batch{b}"] = {"images_per_s": round(b * reps / (ms / 1e3)), "ms_per_batch": round(ms / reps, 4)}
+    out["note"] = "device time per graph replay, CUDA events, L2 flushed between steps"
     return out
 
 
