@@ -128,6 +128,9 @@ __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity
   } while (!done);
 }
 
+#ifndef B2_EARLY_RELEASE  // epilogue returns the accumulator once the last TMEM chunk is loaded
+#define B2_EARLY_RELEASE 1
+#endif
 #ifndef B2_SUSPEND  // 1: TMA, producer and epilogue waits suspend in hardware (the MMA thread polls)
 #define B2_SUSPEND 0
 #endif
@@ -1332,10 +1335,19 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           words[c] = w;
         }
         if (c + 1 < ECH) tmem_wait_ld();
+#if B2_EARLY_RELEASE
+        if (c + 2 == ECH) {  // every chunk is in registers: hand the accumulator back before the last one's math
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+#endif
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (!B2_EARLY_RELEASE || ECH < 2) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
       if constexpr (EM == E_PACK || EM == E_POOLPACK) {
         const int64_t site = POOLED ? (m >> 2) : m;
         const bool writer = mok && (!POOLED || (lane & 3) == 0);
