@@ -399,10 +399,17 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
         if (c + 1 < ECH) tmem_ld32(ta + (c + 1) * 32, vn);
         words[c] = thr_word<true>(v, sthr + (c0 + c) * 16);
         if (c + 1 < ECH) tmem_wait_ld();
+        if (c + 2 == ECH) {  // every chunk is in registers: return the accumulator before the last one's math
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (ECH < 2) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
       const int64_t v = t * BM + r;
       if (v < g.Vtotal) {
         int64_t n;
