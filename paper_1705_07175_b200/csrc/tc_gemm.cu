@@ -428,6 +428,13 @@ inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t 
     const char* e = getenv("B2_PADROW");
     return e ? atoi(e) : B2_PADROW;
   }();
+  // the tile's input band (BM virtual rows plus the window's reach above and
+  // below, padrow_geometry) must fit a band slot and the producer warps;
+  // wider images take the im2col kernel
+  const int64_t band0 = (int64_t)g.pad * (g.W + (g.pad > 0 ? g.pad : 1)) + g.pad;
+  const int64_t r8 = (2 * band0 + BM + 7) / 8 * 8;
+  const int64_t planes = c / 32;
+  if (r8 * 16 * planes > PR_BAND_MAX || r8 * (planes / 4) > 2 * 32 * PR_NPW) return false;
   return on && g.stride == 1 && g.Ho == g.H && g.Wo == g.W && g.kh == g.kw && (g.kh & 1) && g.pad == (g.kh - 1) / 2 &&
          c % 128 == 0 && filters <= 256 && (filters <= 128 ? k <= 1536 : k <= 1280) && g.W < 4096 &&
          (int64_t)g.kh * g.kw * (c / 64) <= 128 &&
