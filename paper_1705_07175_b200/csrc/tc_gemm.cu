@@ -423,18 +423,28 @@ inline void conv_args(Args& g, const void* x, int64_t batch, int h, int w, int c
 #ifndef B2_PADROW
 #define B2_PADROW 1
 #endif
+// Band slot stride: the 16 KB minimum, or the band's planes rounded up to 1 KB.
+inline int padrow_band_bytes(int64_t r8, int64_t planes) {
+  const int64_t need = (r8 * 16 * planes + 1023) / 1024 * 1024;
+  return (int)(need > PR_BAND_MAX ? need : PR_BAND_MAX);
+}
+
 inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t batch) {
   static const int on = [] {
     const char* e = getenv("B2_PADROW");
     return e ? atoi(e) : B2_PADROW;
   }();
   // the tile's input band (BM virtual rows plus the window's reach above and
-  // below, padrow_geometry) must fit a band slot and the producer warps;
+  // below, padrow_geometry) must fit the producer warps, and the band ring
+  // (slots sized by padrow_band_bytes) shared memory next to the weights;
   // wider images take the im2col kernel
   const int64_t band0 = (int64_t)g.pad * (g.W + (g.pad > 0 ? g.pad : 1)) + g.pad;
   const int64_t r8 = (2 * band0 + BM + 7) / 8 * 8;
   const int64_t planes = c / 32;
-  if (r8 * 16 * planes > PR_BAND_MAX || r8 * (planes / 4) > 2 * 32 * PR_NPW) return false;
+  if (r8 * (planes / 4) > 2 * 32 * PR_NPW || r8 * 16 * planes > 128 * 1024) return false;
+  const int bb = padrow_band_bytes(r8, planes);
+  const int nkb = (int)((k + 255) / 256);
+  if ((filters > 128 ? padrow_smem_bytes<256>(nkb, bb) : padrow_smem_bytes<128>(nkb, bb)) > 227 * 1024) return false;
   return on && g.stride == 1 && g.Ho == g.H && g.Wo == g.W && g.kh == g.kw && (g.kh & 1) && g.pad == (g.kh - 1) / 2 &&
          c % 128 == 0 && filters <= 256 && (filters <= 128 ? k <= 1536 : k <= 1280) && g.W < 4096 &&
          (int64_t)g.kh * g.kw * (c / 64) <= 128 &&
@@ -465,15 +475,16 @@ inline void padrow_geometry(PadArgs& p, int64_t batch, int h, int w, int kh, int
 // stream-ordered scratch).  p.nkb, p.P, p.kmmas, p.F, p.thresh/ge set by the caller.
 template <bool BYTEIN>
 inline int padrow_run(PadArgs& p, const int8_t* w, int64_t b_row_bytes, int pool, uint64_t* out, cudaStream_t st) {
-  if ((int64_t)p.R8 * 16 * p.P > PR_BAND_MAX || (int64_t)p.R8 * (BYTEIN ? 1 : p.P / 4) > 2 * 32 * PR_NPW ||
+  if ((int64_t)p.R8 * 16 * p.P > 128 * 1024 || (int64_t)p.R8 * (BYTEIN ? 1 : p.P / 4) > 2 * 32 * PR_NPW ||
       p.N < 0)
     return B2_EINVAL;
+  p.band_bytes = padrow_band_bytes(p.R8, p.P);
   p.ldo32 = 2 * wpl64(p.F);
   const bool wide = p.F > 128;  // one 256-column tile
   if (BYTEIN && wide) return B2_EINVAL;
   CUtensorMap map;
   if (int rc = make_bmap(&map, w, p.F, b_row_bytes, wide ? 256 : 128)) return rc;
-  const int smem = wide ? padrow_smem_bytes<256>(p.nkb) : padrow_smem_bytes<128>(p.nkb);
+  const int smem = wide ? padrow_smem_bytes<256>(p.nkb, p.band_bytes) : padrow_smem_bytes<128>(p.nkb, p.band_bytes);
   static const bool generic_only = getenv("B2_PR_GENERIC") && atoi(getenv("B2_PR_GENERIC"));  // test hook
   const bool k3 = !generic_only && p.kh == 3 && p.kmmas == (BYTEIN ? 1 : 2);  // the unrolled 3x3 issue loops
   void (*kern)(CUtensorMap, PadArgs);

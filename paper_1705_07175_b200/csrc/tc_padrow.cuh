@@ -41,6 +41,7 @@ struct PadArgs {
   int R8;              // band rows (multiple of 8): 128 + 2 * band0
   int band0;           // halo above a tile: pad * Wp + pad virtual rows
   int nkb;             // 128-byte B atoms (256 K elements) in shared memory
+  int band_bytes;      // band slot stride: max(PR_BAND_MAX, R8 * 16 * planes) rounded to 1 KB
   int F;               // filters (<= 128)
   int kmmas;           // K=64 MMAs per window cell (= P / 2)
   uint32_t* out_bits;  // (N*H*W, ldo32) words
@@ -84,7 +85,7 @@ constexpr int PR_NPW = 8;       // producer warps
 constexpr int PR_NEPI = B2_PR_NEPI;  // epilogue warps: 4 (one per lane quarter) or 8 (two, half the columns each)
 constexpr int PR_BANDS = 4;     // band ring (tiles in flight: hides the band loads' DRAM latency)
 constexpr int PR_ACC = 3;       // accumulator buffers (3 x 128 columns + scale columns)
-constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot
+constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot (the minimum; wider images take larger slots)
 
 // KH, KMMAS > 0: compile-time window and K chunks per cell (the issuing
 // thread's 18 descriptor offsets for 3x3 / c = 128 stay in registers and the
@@ -121,8 +122,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sb = smem;                                    // resident weights: nkb atoms of BN x 128 B
-  uint8_t* sband = sb + g.nkb * BN * 128;                // PR_BANDS x PR_BAND_MAX
-  int4* sthr = reinterpret_cast<int4*>(sband + PR_BANDS * PR_BAND_MAX);  // 64 x (mul, add) pairs
+  uint8_t* sband = sb + g.nkb * BN * 128;                // PR_BANDS x band_bytes
+  int4* sthr = reinterpret_cast<int4*>(sband + PR_BANDS * g.band_bytes);  // 64 x (mul, add) pairs
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + BN / 2);
   uint64_t* bres = reinterpret_cast<uint64_t*>(sgm + BN / 32);
   uint64_t* bfull = bres + 1;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
 #endif
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
-        const uint64_t adesc0 = noswz_desc(smem_u32(sband + slot * PR_BAND_MAX), plane_bytes);
+        const uint64_t adesc0 = noswz_desc(smem_u32(sband + slot * g.band_bytes), plane_bytes);
         if constexpr (KH > 0) {
           constexpr int PAD = KH / 2;
 #pragma unroll
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
       const uint32_t cmask = (1u << g.cin) - 1u;
       for (int sl = 0; sl < PR_BANDS; ++sl)  // the zero planes, once
         for (int b = pt; b < g.R8; b += 32 * PR_NPW)
-          *reinterpret_cast<uint4*>(sband + sl * PR_BAND_MAX + plane_bytes + (size_t)b * 16) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(sband + sl * g.band_bytes + plane_bytes + (size_t)b * 16) = make_uint4(0, 0, 0, 0);
       int slot = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
           }
         }
         mbar_wait_suspend(&bempty[slot], ph ^ 1);
-        uint8_t* band = sband + slot * PR_BAND_MAX;
+        uint8_t* band = sband + slot * g.band_bytes;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int b = pt + i * 32 * PR_NPW;
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
         }
       }
       mbar_wait_suspend(&bempty[slot], ph ^ 1);
-      uint8_t* band = sband + slot * PR_BAND_MAX;
+      uint8_t* band = sband + slot * g.band_bytes;
 #pragma unroll
       for (int i = 0; i < UMAX; ++i) {
         const int u = pt + i * 32 * PR_NPW;
@@ -459,8 +460,8 @@ __global__ void k_expand_f4_cells(const uint64_t* __restrict__ w, int64_t rows, 
 }
 
 template <int BNT>
-inline int padrow_smem_bytes(int nkb) {
-  return nkb * BNT * 128 + pr_bands<BNT>() * PR_BAND_MAX + BNT / 2 * 16 + BNT / 8 +
+inline int padrow_smem_bytes(int nkb, int band_bytes) {
+  return nkb * BNT * 128 + pr_bands<BNT>() * band_bytes + BNT / 2 * 16 + BNT / 8 +
          8 * (1 + 2 * pr_bands<BNT>() + 2 * pr_acc<BNT>()) + 16 + 8 * 128 + 1024;  // + MMA offset table (<= 128)
 }
 

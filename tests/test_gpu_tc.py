@@ -93,9 +93,12 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
                                                 (8, 8, 128, 100, True, 240),
                                                 # ... its 256-column variant (one accumulator, 129-256 filters)
                                                 (16, 16, 128, 256, False, 80), (16, 16, 128, 200, True, 80),
-                                                # the widest image whose band fits a padded-row slot, and the
-                                                # first one past it (im2col kernel; the sweep's C=128 64x64 case)
-                                                (62, 62, 128, 128, False, 6), (64, 64, 128, 128, True, 6)])
+                                                # band slots wider than the 16 KB minimum (W > 62): 128- and
+                                                # 256-column variants; the widest image whose band the producer
+                                                # warps cover (W = 190) and the first one past it (im2col kernel)
+                                                (62, 62, 128, 128, False, 6), (64, 64, 128, 128, True, 6),
+                                                (16, 64, 128, 200, True, 20), (8, 190, 128, 64, False, 20),
+                                                (8, 191, 128, 64, False, 20)])
 def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch, fmt):
     rng = np.random.default_rng(5 + h + c + f)
     xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
