@@ -270,9 +270,12 @@ int b2_tc4_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_f4, i
                          b2_thresh th, uint64_t* out, void* stream);
 int b2_tc4_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_f4,
                         int64_t filters, int kh, int kw, int stride, int pad, int32_t* out, void* stream);
-/* For stride-1 same-size convs with c % 128 == 0, <= 128 filters, K <= 1536
- * and enough output rows to fill the GPU, b2_tc4_conv_bn_pack runs the
- * padded-row implicit GEMM; with pool = 1 it then takes a
+/* For stride-1 same-size convs with c % 128 == 0, <= 256 filters (K <= 1536
+ * up to 128 filters, <= 1280 above), a tile's input band the producer warps
+ * cover (c = 128: w <= 190) and weights plus band ring in shared memory, and
+ * enough output rows to fill the GPU, b2_tc4_conv_bn_pack runs the
+ * padded-row implicit GEMM; other convs take the im2col
+ * kernel (same results); with pool = 1 the padded-row path takes a
  * stream-ordered scratch of batch*h*w*ldo words from the device's default
  * memory pool (cudaMallocAsync / cudaFreeAsync on `stream`, capturable into
  * CUDA graphs; the pool's release threshold is raised so the scratch is
