@@ -525,7 +525,7 @@ def bgemm_sweep(dev, flush, sizes=(1024, 2048, 4096, 8192, 16384)):
         ms = timed_graph(lambda: gemm.bgemm_device(a, n, b, n, n // 64, n, c, b_i8=b8), reps, flush)
         ah, bh, got = (_dev.download(a[:16], np.uint64), _dev.download(b[:16], np.uint64),
                        _dev.download(c[:16, :16], np.int32))
-        want = n - 2 * np.bitwise_count(ah[:, None, :] ^ bh[None, :, :]).sum(-1)
+        want = n - 2 * np.bitwise_count(ah[:, None, :] ^ bh[None, :, :]).sum(-1).astype(np.int64)
         lib, _ = measure_fp4_gemm(dev, n, reps=5)
         tops = 2.0 * n ** 3 / (ms / 1e3) / 1e12
         res[str(n)] = {"ms": round(ms, 4), "Gops": round(tops * 1e3), "cublaslt_nvfp4_Gops": round(lib * 1e3) if lib else None,

@@ -239,6 +239,16 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
  * + bit im2col (_kernels.py:170-199) of every output pixel into `scratch`
  * (b2_tc_byte_conv_scratch_bytes bytes: window bits plus a validity mask,
  * padding cells invalid), then the tensor-core GEMM with zero padding. */
+/* Kernel b2_tc_byte_conv_bn_pack (int8 weights) runs for these arguments:
+ * 1 = the fused first-layer kernel (one launch, `scratch` unused): stride 1,
+ * odd kh == kw with pad = (kh - 1) / 2, c <= 3, kh*kw*c <= 31, <= 256 filters,
+ * no pool, w a power of two dividing 128, h*w a multiple of 128, and an
+ * image row of w*c bytes that is a multiple of 16 and at most 256; the
+ * window and the output threshold go through ONE int8 MMA per 128 pixels;
+ * 0 = the byte unroll into `scratch` + the tensor-core GEMM (two launches);
+ * -1 = invalid arguments.  B2_BYTECONV_FUSED=0 disables the fused kernel. */
+int b2_tc_byte_conv_path(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad,
+                         int pool);
 int64_t b2_tc_byte_conv_scratch_bytes(int64_t batch, int h, int w, int c, int kh, int kw, int stride, int pad);
 int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_thresh th_in,
                             const int8_t* w_i8, int64_t filters, int kh, int kw, int stride, int pad, int pool,
@@ -270,16 +280,26 @@ int b2_tc4_dense_bn_pack(const uint64_t* x, int64_t batch, const int8_t* w_f4, i
                          b2_thresh th, uint64_t* out, void* stream);
 int b2_tc4_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_f4,
                         int64_t filters, int kh, int kw, int stride, int pad, int32_t* out, void* stream);
-/* For stride-1 same-size convs with c % 128 == 0, <= 256 filters (K <= 1536
- * up to 128 filters, <= 1280 above), a tile's input band the producer warps
- * cover (c = 128: w <= 190) and weights plus band ring in shared memory, and
- * enough output rows to fill the GPU, b2_tc4_conv_bn_pack runs the
- * padded-row implicit GEMM; other convs take the im2col
- * kernel (same results); with pool = 1 the padded-row path takes a
- * stream-ordered scratch of batch*h*w*ldo words from the device's default
- * memory pool (cudaMallocAsync / cudaFreeAsync on `stream`, capturable into
- * CUDA graphs; the pool's release threshold is raised so the scratch is
- * reused).  B2_PADROW=0 in the environment disables it. */
+/* Kernel choice of b2_tc4_conv_bn_pack (same results on every path; the
+ * call allocates nothing):
+ *  - stride-1 same-size convs with odd kh == kw, pad = (kh - 1) / 2,
+ *    c % 128 == 0, <= 256 filters, w a power of two dividing 128, h*w a
+ *    multiple of 128 (pooled: 128 / w even), weights plus >= 2 band slots in
+ *    shared memory and >= one 128-pixel tile per SM: the ROW-ALIGNED
+ *    padded-row implicit GEMM, pooling fused into its epilogue (DESIGN.md
+ *    §3.1b);
+ *  - otherwise unpooled stride-1 same-size convs with c % 128 == 0, <= 256
+ *    filters (K <= 1536 up to 128 filters, <= 1280 above), a band the producer
+ *    warps cover (c = 128: w <= 190), weights resident, and enough virtual
+ *    rows to fill the GPU: the virtual-grid padded-row kernel;
+ *  - everything else: the implicit-im2col kernel (pool fused in its epilogue),
+ *    or cluster split-K for few-tile launches with deep K.
+ * B2_PADROW=0 / B2_PADROW_ALIGN=0 in the environment disable the padded-row
+ * kernels.  b2_tc4_conv_path returns the path a call with these arguments
+ * takes: 0 im2col, 1 split-K, 2 padded-row, 3 row-aligned padded-row (-1:
+ * invalid arguments). */
+int b2_tc4_conv_path(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad,
+                     int pool);
 int b2_tc4_conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, const int8_t* w_f4,
                         int64_t filters, int kh, int kw, int stride, int pad, int pool, b2_thresh th, uint64_t* out,
                         void* stream);

@@ -72,6 +72,8 @@ SIGNATURES = {
     "b2_tc_byte_conv_bn_pack": (cint, [vp, i64, cint, cint, cint, Thresh, vp, i64, cint, cint, cint, cint, cint,
                                        Thresh, vp, vp, vp]),
     "b2_f4_kpad": (i64, [i64]),
+    "b2_tc_byte_conv_path": (cint, [i64, cint, cint, cint, i64, cint, cint, cint, cint, cint]),
+    "b2_tc4_conv_path": (cint, [i64, cint, cint, cint, i64, cint, cint, cint, cint, cint]),
     "b2_expand_f4": (cint, [vp, i64, i64, i64, vp, vp]),
     "b2_f4_cells_row_bytes": (i64, [cint]),
     "b2_expand_f4_cells": (cint, [vp, i64, i64, cint, cint, vp, vp]),

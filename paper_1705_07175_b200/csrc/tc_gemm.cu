@@ -9,6 +9,7 @@
 
 #include "tc_i8.cuh"
 #include "tc_padrow.cuh"
+#include "tc_byteconv.cuh"
 
 #ifndef B2_RESIDENT_B
 #define B2_RESIDENT_B 1
@@ -429,6 +430,34 @@ inline int padrow_band_bytes(int64_t r8, int64_t planes) {
   return (int)(need > PR_BAND_MAX ? need : PR_BAND_MAX);
 }
 
+// Shared padded-row geometry (virtual grid W + pad wide, H + pad tall per image).
+inline void padrow_geometry(PadArgs& p, int64_t batch, int h, int w, int kh, int kw, int pad) {
+  p.N = (int)batch;
+  p.H = h;
+  p.W = w;
+  p.kh = kh;
+  p.kw = kw;
+  p.pad = pad;
+  // pad zero columns per row and pad zero rows per image: a window reaching
+  // pad cells past any edge lands on zeros
+  p.Wp = w + (pad > 0 ? pad : 1);
+  p.VI = (int64_t)(h + (pad > 0 ? pad : 1)) * p.Wp;
+  p.Vtotal = p.VI * batch;
+  // ceil(2^64 / VI) and ceil(2^32 / Wp): multiply-high division (vsplit) is
+  // exact while v * ((-2^64) mod VI) < 2^64 and rem * ((-2^32) mod Wp) < 2^32
+  // for every virtual row v and remainder rem < VI; padrow_exact checks the
+  // sufficient bounds Vtotal * VI < 2^64 and VI * Wp < 2^32
+  p.vi_magic = ~0ull / (uint64_t)p.VI + 1;
+  p.wp_magic = (uint32_t)((((uint64_t)1 << 32) + p.Wp - 1) / p.Wp);
+  p.band0 = pad * p.Wp + pad;  // the window's reach above (and below) a virtual row
+  p.R8 = ((2 * p.band0 + BM) + 7) / 8 * 8;
+}
+
+inline bool padrow_exact(const PadArgs& p) {
+  return (unsigned __int128)p.Vtotal * (unsigned __int128)p.VI < ((unsigned __int128)1 << 64) &&
+         (uint64_t)p.VI * (uint64_t)p.Wp < ((uint64_t)1 << 32);
+}
+
 inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t batch) {
   static const int on = [] {
     const char* e = getenv("B2_PADROW");
@@ -445,6 +474,11 @@ inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t 
   const int bb = padrow_band_bytes(r8, planes);
   const int nkb = (int)((k + 255) / 256);
   if ((filters > 128 ? padrow_smem_bytes<256>(nkb, bb) : padrow_smem_bytes<128>(nkb, bb)) > 227 * 1024) return false;
+  {
+    PadArgs p{};
+    padrow_geometry(p, batch, g.H, g.W, g.kh, g.kw, g.pad);
+    if (!padrow_exact(p)) return false;  // e.g. a 4000 x 4000 1x1 conv: the index split would not be exact
+  }
   return on && g.stride == 1 && g.Ho == g.H && g.Wo == g.W && g.kh == g.kw && (g.kh & 1) && g.pad == (g.kh - 1) / 2 &&
          c % 128 == 0 && filters <= 256 && (filters <= 128 ? k <= 1536 : k <= 1280) && g.W < 4096 &&
          (int64_t)g.kh * g.kw * (c / 64) <= 128 &&
@@ -452,31 +486,70 @@ inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t 
          (int64_t)(g.H + 1) * (g.W + 1) * batch >= (int64_t)BM * num_sms();
 }
 
-// Shared padded-row geometry (virtual grid W + pad wide, H + pad tall per image).
-inline void padrow_geometry(PadArgs& p, int64_t batch, int h, int w, int kh, int kw, int pad) {
+// Row-aligned padded-row plan (tc_padrow.cuh ALIGN): tiles of 128 pixels
+// covering whole rows of one image, kw column-shifted copies of the band,
+// pooling fused into the epilogue.  Fills p (geometry, band ring, smem) and
+// returns false when the layer does not qualify.  One routine decides
+// eligibility and shapes the launch, so the two cannot drift apart.
+#ifndef B2_PADROW_ALIGN
+#define B2_PADROW_ALIGN 1
+#endif
+inline bool padrow_align_plan(const Args& g, int c, int64_t filters, int64_t k, int64_t batch, int pool, PadArgs& p,
+                              int& smem) {
+  static const int on = [] {
+    const char* e = getenv("B2_PADROW_ALIGN");
+    return e ? atoi(e) : B2_PADROW_ALIGN;
+  }();
+  static const int min_bands = [] {
+    const char* e = getenv("B2_ALIGN_MIN_BANDS");
+    return e ? atoi(e) : 2;
+  }();
+  const int w = g.W, h = g.H;
+  if (!on || g.stride != 1 || g.Ho != h || g.Wo != w || g.kh != g.kw || !(g.kh & 1) || g.pad != (g.kh - 1) / 2 ||
+      c % 128 || filters > 256 || w < 1 || (w & (w - 1)) || BM % w || ((int64_t)h * w) % BM || batch > INT32_MAX)
+    return false;
+  const int tr = BM / w;  // image rows per tile
+  if (pool && (tr & 1)) return false;
+  if ((int64_t)g.kh * g.kw * (c / 64) > 128) return false;  // MMA offset table
+  if (batch * h * w / BM < num_sms()) return false;          // too few tiles to fill the GPU
+  p = PadArgs{};
   p.N = (int)batch;
   p.H = h;
   p.W = w;
-  p.kh = kh;
-  p.kw = kw;
-  p.pad = pad;
-  // pad zero columns per row and pad zero rows per image: a window reaching
-  // pad cells past any edge lands on zeros
-  p.Wp = w + (pad > 0 ? pad : 1);
-  p.VI = (int64_t)(h + (pad > 0 ? pad : 1)) * p.Wp;
-  p.Vtotal = p.VI * batch;
-  p.vi_magic = ~0ull / (uint64_t)p.VI + 1;  // ceil(2^64 / VI), exact multiply-high division for v < 2^40
-  p.wp_magic = (uint32_t)((((uint64_t)1 << 32) + p.Wp - 1) / p.Wp);
-  p.band0 = pad * p.Wp + pad;  // the window's reach above (and below) a virtual row
-  p.R8 = ((2 * p.band0 + BM) + 7) / 8 * 8;
+  p.kh = g.kh;
+  p.kw = g.kw;
+  p.pad = g.pad;
+  p.HW = (int64_t)h * w;
+  p.wshift = 0;
+  while ((1 << p.wshift) < w) ++p.wshift;
+  p.Rb = (tr + 2 * g.pad) * w;
+  p.R8 = (p.Rb + 7) / 8 * 8;
+  p.P = c / 32;
+  if ((int64_t)p.Rb * (p.P / 4) > 2 * 32 * PR_NPW) return false;  // band units per producer thread
+  const int64_t band = ((int64_t)p.R8 * 16 * g.kw * p.P + 1023) / 1024 * 1024;
+  if (band > 128 * 1024) return false;
+  p.band_bytes = (int)band;
+  p.nkb = (int)((k + 255) / 256);
+  p.kmmas = p.P / 2;
+  p.F = (int)filters;
+  p.pool = pool;
+  for (p.nbands = PR_BANDS_MAX; p.nbands >= min_bands; --p.nbands) {
+    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0)
+                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0);
+    if (smem <= 227 * 1024) return true;
+  }
+  return false;
 }
 
-// Launch the padded-row kernel (and, pooled, the bit-pool pass on a
-// stream-ordered scratch).  p.nkb, p.P, p.kmmas, p.F, p.thresh/ge set by the caller.
+
+
+// Launch the padded-row kernel (and, pooled — only the opt-in byte-input
+// entry b2_tc4_byte_conv_padrow — the bit-pool pass on a stream-ordered
+// scratch).  p.nkb, p.P, p.kmmas, p.F, p.thresh/ge set by the caller.
 template <bool BYTEIN>
 inline int padrow_run(PadArgs& p, const int8_t* w, int64_t b_row_bytes, int pool, uint64_t* out, cudaStream_t st) {
   if ((int64_t)p.R8 * 16 * p.P > 128 * 1024 || (int64_t)p.R8 * (BYTEIN ? 1 : p.P / 4) > 2 * 32 * PR_NPW ||
-      p.N < 0)
+      p.N < 0 || !padrow_exact(p))
     return B2_EINVAL;
   p.band_bytes = padrow_band_bytes(p.R8, p.P);
   p.ldo32 = 2 * wpl64(p.F);
@@ -515,7 +588,7 @@ inline int padrow_run(PadArgs& p, const int8_t* w, int64_t b_row_bytes, int pool
       }
       pool_kept.fetch_or(1ull << (dev & 63));
     }
-    if (cudaMallocAsync(&scratch, (size_t)p.N * p.H * p.W * p.ldo32 * 4, st) != cudaSuccess) return launched();
+    if (cudaError_t e = cudaMallocAsync(&scratch, (size_t)p.N * p.H * p.W * p.ldo32 * 4, st)) return (int)e;
     p.out_bits = reinterpret_cast<uint32_t*>(scratch);
   } else {
     p.out_bits = reinterpret_cast<uint32_t*>(out);
@@ -534,6 +607,31 @@ inline int padrow_run(PadArgs& p, const int8_t* w, int64_t b_row_bytes, int pool
   return rc;
 }
 
+// Launch the row-aligned kernel planned by padrow_align_plan (pool fused).
+inline int padrow_align_run(PadArgs& p, int smem, const void* lines, int sstride, const int8_t* w, int64_t b_row_bytes,
+                            const b2_thresh& th, uint64_t* out, cudaStream_t st) {
+  p.x = reinterpret_cast<const uint32_t*>(lines);
+  p.sstride = sstride;
+  p.thresh = th.thresh;
+  p.ge = th.ge_dir;
+  p.ldo32 = 2 * wpl64(p.F);
+  p.out_bits = reinterpret_cast<uint32_t*>(out);
+  const bool wide = p.F > 128;
+  CUtensorMap map;
+  if (int rc = make_bmap(&map, w, p.F, b_row_bytes, wide ? 256 : 128)) return rc;
+  static const bool generic_only = getenv("B2_PR_GENERIC") && atoi(getenv("B2_PR_GENERIC"));  // test hook
+  const bool k3 = !generic_only && p.kh == 3 && p.kmmas == 2;
+  void (*kern)(CUtensorMap, PadArgs) =
+      wide ? (k3 ? k_padrow_conv<3, 2, 256, false, true> : k_padrow_conv<0, 0, 256, false, true>)
+           : (k3 ? k_padrow_conv<3, 2, 128, false, true> : k_padrow_conv<0, 0, 128, false, true>);
+  static std::atomic<uint64_t> attr[4];
+  smem_optin(kern, 227 * 1024, attr[(wide ? 2 : 0) + (k3 ? 1 : 0)]);
+  const int64_t tiles = (int64_t)p.N * p.HW / BM;
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  launch_k(kern, grid, 32 * (4 + PR_NPW + (wide ? pr_nepi<256, true>() : pr_nepi<128, true>())), smem, st, map, p);
+  return launched();
+}
+
 inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c, const int8_t* w_f4, int64_t filters,
                          int64_t k, int pool, uint64_t* out, cudaStream_t st) {
   if (batch > INT32_MAX) return B2_EINVAL;
@@ -548,6 +646,21 @@ inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c,
   p.thresh = g.thresh;
   p.ge = g.ge;
   return padrow_run<false>(p, w_f4, kpad_f4(k) / 2, pool, out, st);
+}
+
+// Kernel choice of the fused fp4 conv (b2_tc4_conv_bn_pack), also exported
+// as b2_tc4_conv_path so tests can assert which kernel a case exercised.
+enum ConvPath { PATH_IM2COL = 0, PATH_SPLITK = 1, PATH_PADROW = 2, PATH_PADROW_ALIGNED = 3 };
+inline int conv_path_f4(const Args& g, int c, int64_t filters, int64_t k, int64_t batch, int pool, PadArgs& p,
+                        int& smem) {
+  if (!batch) return PATH_IM2COL;
+  if (splitk_count<A_CONV, E_PACK>(g, k)) return PATH_SPLITK;
+  if (padrow_align_plan(g, c, filters, k, batch, pool, p, smem)) return PATH_PADROW_ALIGNED;
+  // pooled layers the row-aligned kernel cannot take use the im2col kernel's
+  // fused pool: the virtual grid's pool windows straddle tiles, and an
+  // unpooled scratch would be an allocation inside the forward pass
+  if (!pool && padrow_ok(g, c, filters, k, batch)) return PATH_PADROW;
+  return PATH_IM2COL;
 }
 
 inline void pack_args(Args& g, const b2_thresh& th, uint64_t* out, int64_t n) {
@@ -633,11 +746,88 @@ int conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, cons
   g.N = (int)filters;
   pack_args(g, th, out, filters);
   if constexpr (F4) {
-    if (batch && !splitk_count<A_CONV, E_PACK>(g, k) && padrow_ok(g, c, filters, k, batch))
-      return padrow_launch(g, lines, batch, c, w_i8, filters, k, pool, out, S(stream));
+    PadArgs p;
+    int smem = 0;
+    switch (conv_path_f4(g, c, filters, k, batch, pool, p, smem)) {
+      case PATH_PADROW_ALIGNED: return padrow_align_run(p, smem, lines, g.sstride, w_i8, kpad_f4(k) / 2, th, out, S(stream));
+      case PATH_PADROW: return padrow_launch(g, lines, batch, c, w_i8, filters, k, pool, out, S(stream));
+      default: break;
+    }
   }
   if (pool) return launch<A_CONV, E_POOLPACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
   return launch<A_CONV, E_PACK, F4>(g, w_i8, kpad_for<F4>(k), S(stream), k);
+}
+
+// Fused first layer (tc_byteconv.cuh): row-aligned tiles, window K <= 31
+// bits (+ the folded threshold) in one int8 MMA, no unrolled scratch.
+#ifndef B2_BYTECONV_FUSED
+#define B2_BYTECONV_FUSED 1
+#endif
+inline bool byteconv_fused_ok(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad,
+                              int pool) {
+  static const int on = [] {
+    const char* e = getenv("B2_BYTECONV_FUSED");
+    return e ? atoi(e) : B2_BYTECONV_FUSED;
+  }();
+  if (!on || pool || stride != 1 || kh != kw || !(kh & 1) || pad != (kh - 1) / 2 || c < 1 || c > 3 ||
+      (int64_t)kh * kw * c > 31 || filters < 1 || filters > 256 || w < 1 || (w & (w - 1)) || BM % w ||
+      ((int64_t)h * w) % BM || batch < 1 || batch * h * w >= ((int64_t)1 << 31))
+    return false;
+  // the tile's code band, and its raw rows as one TMA box (row pitch a multiple
+  // of 16 bytes, at most 256 bytes wide)
+  const int64_t rowb = (int64_t)w * c, brows = BM / w + 2 * pad;
+  return brows * w <= 1024 && rowb % 16 == 0 && rowb <= 256 && brows <= 256 && brows * rowb <= BC_RAW_BYTES;
+}
+
+inline int byteconv_fused_run(const uint8_t* x, int64_t batch, int h, int w, int c, const b2_thresh& th_in,
+                              const int8_t* w_i8, int64_t filters, int kh, int kw, int pad, const b2_thresh& th_out,
+                              uint64_t* out, cudaStream_t st) {
+  ByteConvArgs g{};
+  g.x = x;
+  g.N = (int)batch;
+  g.H = h;
+  g.W = w;
+  g.c = c;
+  g.kh = kh;
+  g.kw = kw;
+  g.pad = pad;
+  g.HW = (int64_t)h * w;
+  g.tpi = (uint32_t)(g.HW / BM);
+  while ((1 << g.wshift) < w) ++g.wshift;
+  g.K = kh * kw * c;
+  g.th_in = th_in.thresh;
+  g.ge_in = th_in.ge_dir;
+  g.w = w_i8;
+  g.wpitch = kpad_of(g.K);
+  g.F = (int)filters;
+  g.thresh = th_out.thresh;
+  g.ge = th_out.ge_dir;
+  g.out_bits = reinterpret_cast<uint32_t*>(out);
+  g.ldo32 = 2 * wpl64(filters);
+  // the image as (N*H rows) x (W*c bytes) for the producers' band TMA
+  auto fn = encode_fn();
+  if (!fn) return B2_EINVAL;
+  CUtensorMap xmap;
+  cuuint64_t dims[2] = {(cuuint64_t)w * c, (cuuint64_t)batch * h};
+  cuuint64_t strides[1] = {(cuuint64_t)w * c};
+  cuuint32_t box[2] = {(cuuint32_t)(w * c), (cuuint32_t)(BM / w + 2 * pad)};
+  cuuint32_t estr[2] = {1, 1};
+  if (fn(&xmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(x), dims, strides, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return B2_EINVAL;
+  const bool wide = filters > 128, k3 = kh == 3 && w <= 32;  // row triples by shuffle: a row within one warp
+  // the 3x3 / 3-channel first layer (RGB images) with compile-time channels
+  void (*kern)(CUtensorMap, ByteConvArgs) =
+      wide ? (k3 ? (c == 3 ? k_byteconv<256, 3, 3> : k_byteconv<256, 3>) : k_byteconv<256, 0>)
+           : (k3 ? (c == 3 ? k_byteconv<128, 3, 3> : k_byteconv<128, 3>) : k_byteconv<128, 0>);
+  const int smem = wide ? bc_smem_bytes<256>() : bc_smem_bytes<128>();
+  static std::atomic<uint64_t> attr[6];
+  smem_optin(kern, smem, attr[(wide ? 3 : 0) + (k3 ? (c == 3 ? 2 : 1) : 0)]);
+  const int64_t tiles = batch * g.HW / BM;
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  launch_k(kern, grid, 32 * (4 + BC_NPW + BC_NEPI), smem, st, xmap, g);
+  return launched();
 }
 
 template <bool F4>
@@ -651,6 +841,8 @@ int byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c, b2_t
   conv_args(g, x, batch, h, w, c, kh, kw, stride, pad);
   if (pool && ((g.Ho & 1) || (g.Wo & 1))) return B2_EINVAL;
   if (!batch) return 0;
+  if (!F4 && byteconv_fused_ok(batch, h, w, c, filters, kh, kw, stride, pad, pool))
+    return byteconv_fused_run(x, batch, h, w, c, th_in, w_i8, filters, kh, kw, pad, th_out, out, S(stream));
   const int64_t k = (int64_t)kh * kw * c;
   const int kw32 = (int)((k + 31) / 32);
   {
@@ -802,6 +994,23 @@ int b2_tc_input8_bn_pack(const uint8_t* x, int64_t batch, int64_t k, const int8_
       return tc::launch<tc::A_BYTES_TMA, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k, &amap);
   }
   return tc::launch<tc::A_BYTES, tc::E_PACK>(g, w_i8, tc::kpad_of(k), S(stream), k);
+}
+
+int b2_tc4_conv_path(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad,
+                     int pool) {
+  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || c % 64) return -1;
+  tc::Args g{};
+  tc::conv_args(g, nullptr, batch, h, w, c, kh, kw, stride, pad);
+  g.N = (int)filters;
+  tc::PadArgs p;
+  int smem = 0;
+  return tc::conv_path_f4(g, c, filters, (int64_t)kh * kw * c, batch, pool, p, smem);
+}
+
+int b2_tc_byte_conv_path(int64_t batch, int h, int w, int c, int64_t filters, int kh, int kw, int stride, int pad,
+                         int pool) {
+  if (!tc::conv_ok(batch, h, w, c, filters, kh, kw, stride, pad) || c > 8 || (int64_t)kh * kw * c > tc::BK) return -1;
+  return tc::byteconv_fused_ok(batch, h, w, c, filters, kh, kw, stride, pad, pool) ? 1 : 0;
 }
 
 int64_t b2_tc_byte_conv_scratch_bytes(int64_t batch, int h, int w, int c, int kh, int kw, int stride, int pad) {

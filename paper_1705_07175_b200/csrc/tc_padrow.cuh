@@ -54,6 +54,17 @@ struct PadArgs {
   int cin;
   const int32_t* th_in;
   const uint8_t* ge_in;
+  // ALIGN (row-aligned tiles): a tile is 128 consecutive pixels of one image
+  // (128 / W whole rows, W | 128, 128 | H W); the band holds kw copies of the
+  // tile's input rows (+-pad rows), copy dx shifted by dx - pad columns with
+  // zeros past the row ends, so window cell (dy, dx) is copy dx at a shift
+  // of dy W rows: no virtual zero column / row, and a 2x2 pool window lies
+  // inside one tile (fused into the epilogue)
+  int64_t HW;          // pixels per image
+  int wshift;          // log2 W
+  int Rb;              // band rows per copy: (128 / W + 2 pad) W
+  int nbands;          // band slots in the ring (<= PR_BANDS_MAX)
+  int pool;            // fused 2x2/2 max-pool (OR ge / AND le of thresholded bits)
 };
 
 #ifndef B2_PADROW_LBO_K
@@ -86,6 +97,7 @@ constexpr int PR_NEPI = B2_PR_NEPI;  // epilogue warps: 4 (one per lane quarter)
 constexpr int PR_BANDS = 4;     // band ring (tiles in flight: hides the band loads' DRAM latency)
 constexpr int PR_ACC = 3;       // accumulator buffers (3 x 128 columns + scale columns)
 constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot (the minimum; wider images take larger slots)
+constexpr int PR_BANDS_MAX = 4;         // barrier slots reserved for the band ring
 
 // KH, KMMAS > 0: compile-time window and K chunks per cell (the issuing
 // thread's 18 descriptor offsets for 3x3 / c = 128 stay in registers and the
@@ -95,9 +107,9 @@ constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot (the minimum; wid
 // band slots; BNT = 256 (up to 256 filters, weights <= 160 KB): one
 // 256-column accumulator (2 x 256 + the scale columns exceed TMEM), eight
 // epilogue warps, three band slots.
-template <int BNT>
-constexpr int pr_nepi() {
-  return BNT == 256 ? 8 : PR_NEPI;
+template <int BNT, bool ALIGN = false>
+constexpr int pr_nepi() {  // row-aligned 128-column tiles: two warps per lane quarter, 64 columns each
+  return BNT == 256 ? 8 : (ALIGN ? 8 : PR_NEPI);
 }
 template <int BNT>
 constexpr int pr_acc() {
@@ -108,13 +120,14 @@ constexpr int pr_bands() {
   return BNT == 256 ? 3 : PR_BANDS;
 }
 
-template <int KH, int KMMAS, int BNT, bool BYTEIN = false>
-__global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
+template <int KH, int KMMAS, int BNT, bool BYTEIN = false, bool ALIGN = false>
+__global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
   constexpr int BN = BNT;
-  constexpr int PR_NEPI = pr_nepi<BNT>();
+  constexpr int PR_NEPI = pr_nepi<BNT, ALIGN>();
   constexpr int PR_ACC = pr_acc<BNT>();
-  constexpr int PR_BANDS = pr_bands<BNT>();
+  static_assert(!(ALIGN && BYTEIN), "row-aligned tiles take packed-bit input");
+  const int PR_BANDS = ALIGN ? g.nbands : pr_bands<BNT>();
   constexpr uint32_t IDESC = idesc_f4(BN);
   constexpr int EPI0 = 4 + PR_NPW;
   constexpr int ACC_COLS = BN;
@@ -127,14 +140,15 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + BN / 2);
   uint64_t* bres = reinterpret_cast<uint64_t*>(sgm + BN / 32);
   uint64_t* bfull = bres + 1;
-  uint64_t* bempty = bfull + PR_BANDS;
-  uint64_t* tfull = bempty + PR_BANDS;
+  uint64_t* bempty = bfull + PR_BANDS_MAX;
+  uint64_t* tfull = bempty + PR_BANDS_MAX;
   uint64_t* tempty = tfull + PR_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + PR_ACC);
   uint2* soff = reinterpret_cast<uint2*>(tmem_slot + 2);  // per MMA: (A, B) descriptor address offsets (16 B units)
+  uint2* spool = soff + 128;  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND) of horizontal pairs
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tiles = (g.Vtotal + BM - 1) / BM;
+  const int64_t tiles = ALIGN ? (int64_t)g.N * g.HW / BM : (g.Vtotal + BM - 1) / BM;
   const uint32_t plane_bytes = (uint32_t)g.R8 * 16u;
 
   if (warp == 0 && lane == 0) {
@@ -184,11 +198,13 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
       int nmma = 0;
       for (int cy = 0; cy < g.kh; ++cy)
         for (int cx = 0; cx < g.kw; ++cx) {
-          const int off = g.band0 + (cy - g.pad) * g.Wp + (cx - g.pad);  // band row of tile row 0
+          // band row of tile row 0 (ALIGN: copy cx, cy rows of W down)
+          const int off = ALIGN ? (cy << g.wshift) : g.band0 + (cy - g.pad) * g.Wp + (cx - g.pad);
+          const int plane0 = ALIGN ? cx * g.P : 0;
           const int cell = cy * g.kw + cx;
           for (int kc = 0; kc < g.kmmas; ++kc, ++nmma) {
             const int k = cell * g.P * 32 + kc * 64;  // K element
-            soff[nmma] = make_uint2(((uint32_t)(2 * kc) * plane_bytes + (uint32_t)off * 16u) >> 4,
+            soff[nmma] = make_uint2(((uint32_t)(plane0 + 2 * kc) * plane_bytes + (uint32_t)off * 16u) >> 4,
                                     (uint32_t)((k >> 8) * BN * 128 + ((k & 255) >> 6) * 32) >> 4);
           }
         }
@@ -225,8 +241,9 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
               for (int kc = 0; kc < KMMAS; ++kc) {
                 const int cell = cy * KH + cx;
                 const int k = (cell * KMMAS + kc) * 64;  // K element (c = 32 * 2 * KMMAS)
-                const uint32_t off = (uint32_t)(g.band0 + (cy - PAD) * g.Wp + (cx - PAD));
-                const uint32_t ao = ((uint32_t)(2 * kc) * plane_bytes + off * 16u) >> 4;
+                const uint32_t off = ALIGN ? (uint32_t)(cy << g.wshift) : (uint32_t)(g.band0 + (cy - PAD) * g.Wp + (cx - PAD));
+                const uint32_t plane = ALIGN ? (uint32_t)(cx * 2 * KMMAS + 2 * kc) : (uint32_t)(2 * kc);
+                const uint32_t ao = (plane * plane_bytes + off * 16u) >> 4;
                 const uint32_t bo = (uint32_t)((k >> 8) * BN * 128 + ((k & 255) >> 6) * 32) >> 4;
                 tc_mma_f4(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
                           (cell | kc) ? 1u : 0u);
@@ -307,6 +324,101 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
         if (lane == 0) mbar_arrive(&bfull[slot]);
         if (++slot == PR_BANDS) slot = 0, ph ^= 1;
       }
+    } else if constexpr (ALIGN) {
+      // row-aligned tiles: unit = (band row b, 4-word group); the input pixel
+      // of band row b (input row y0 - pad + b / W, column b % W) is expanded
+      // once and stored into each copy dx at row b - dx + pad (the copy's
+      // column x' = x - dx + pad must lie in the row).  Copy rows that no
+      // pixel maps to (x' + dx - pad outside the row) stay zero from the
+      // one-time clear below; rows above / below the image are stored as
+      // zeros.  The next tile's loads are issued before this tile's band is
+      // written (register double buffer), so their latency overlaps.
+      constexpr int UMAX = 2;
+      const int pt = (warp - 4) * 32 + lane;  // 0 .. 255
+      const int groups = g.P / 4;
+      const int units = g.Rb * groups;
+      const int kwc = KH > 0 ? KH : g.kw;
+      const int wmask = (1 << g.wshift) - 1;
+      for (int i = pt; i < PR_BANDS * g.band_bytes / 16; i += 32 * PR_NPW)
+        reinterpret_cast<uint4*>(sband)[i] = make_uint4(0, 0, 0, 0);
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * PR_NPW) : "memory");  // the clear lands before any copy row is stored
+      auto load_tile = [&](int64_t t, uint4 (&w)[UMAX], bool (&ok)[UMAX]) {
+        const int64_t p0 = t * BM;
+        const int64_t n = p0 / g.HW;
+        const int y0 = (int)((p0 - n * g.HW) >> g.wshift);
+        const uint32_t* img = g.x + n * g.HW * g.sstride;
+#pragma unroll
+        for (int i = 0; i < UMAX; ++i) {
+          const int u = pt + i * 32 * PR_NPW;
+          ok[i] = false;
+          w[i] = make_uint4(0, 0, 0, 0);
+          if (t < tiles && u < units) {
+            const int b = u / groups, grp = u - b * groups;
+            const int y = y0 - g.pad + (b >> g.wshift);
+            if ((unsigned)y < (unsigned)g.H) {
+              ok[i] = true;
+              w[i] = __ldg(reinterpret_cast<const uint4*>(img + ((int64_t)(y << g.wshift) + (b & wmask)) * g.sstride +
+                                                          4 * grp));
+            }
+          }
+        }
+      };
+      // one thread pulls the inputs of the tile PF_AHEAD steps ahead into L2
+      // (a tile's input rows are one contiguous range of the image)
+      constexpr int PF_AHEAD = 4;
+      auto prefetch = [&](int64_t t) {
+        if (pt != 0 || t >= tiles) return;
+        const int64_t p0 = t * BM, n = p0 / g.HW;
+        const int64_t lo = p0 - n * g.HW - (int64_t)g.pad * g.W, hi = lo + g.Rb;
+        const int64_t l0 = lo < 0 ? 0 : lo, h0 = hi > g.HW ? g.HW : hi;
+        l2_prefetch(g.x + (n * g.HW + l0) * g.sstride, (uint32_t)((h0 - l0) * g.sstride * 4));
+      };
+      for (int i = 1; i < PF_AHEAD; ++i) prefetch(blockIdx.x + (int64_t)i * gridDim.x);
+      int slot = 0;
+      uint32_t ph = 0;
+      uint4 wa[UMAX], wb[UMAX];
+      bool oka[UMAX], okb[UMAX];
+      load_tile(blockIdx.x, wa, oka);
+      // one tile from (wc, okc), loaded one tile earlier; the next tile's
+      // loads go into (wn, okn) while this one is stored
+      auto tile = [&](int64_t t, uint4 (&wc)[UMAX], bool (&okc)[UMAX], uint4 (&wn)[UMAX], bool (&okn)[UMAX]) {
+        prefetch(t + (int64_t)PF_AHEAD * gridDim.x);
+        load_tile(t + gridDim.x, wn, okn);
+        mbar_wait_suspend(&bempty[slot], ph ^ 1);
+        uint8_t* band = sband + slot * g.band_bytes;
+#pragma unroll
+        for (int i = 0; i < UMAX; ++i) {
+          const int u = pt + i * 32 * PR_NPW;
+          if (u < units) {
+            const int b = u / groups, grp = u - b * groups;
+            const int x = b & wmask;
+            uint32_t o[16];
+            widen_f4(wc[i].x, okc[i], o);
+            widen_f4(wc[i].y, okc[i], o + 4);
+            widen_f4(wc[i].z, okc[i], o + 8);
+            widen_f4(wc[i].w, okc[i], o + 12);
+#pragma unroll 3
+            for (int dx = 0; dx < kwc; ++dx) {
+              const int xp = x - dx + g.pad;
+              if ((unsigned)xp < (unsigned)(wmask + 1)) {
+                uint8_t* row = band + (size_t)(dx * g.P + 4 * grp) * plane_bytes + (size_t)(b - dx + g.pad) * 16;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  *reinterpret_cast<uint4*>(row + (size_t)j * plane_bytes) =
+                      make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+              }
+            }
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bfull[slot]);
+        if (++slot == PR_BANDS) slot = 0, ph ^= 1;
+      };
+      for (int64_t t = blockIdx.x; t < tiles; t += 2 * (int64_t)gridDim.x) {
+        tile(t, wa, oka, wb, okb);
+        if (t + gridDim.x < tiles) tile(t + gridDim.x, wb, okb, wa, oka);
+      }
     } else {
     // each thread owns up to UMAX (band row, 4-word group) units per tile;
     // a tile's loads are issued before waiting for its band slot
@@ -380,6 +492,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
     epi_bar<PR_NEPI>();
     int acc = 0;
     uint32_t aph = 0;
+    uint32_t it = 0;  // tiles done by this CTA (ALIGN pool buffer parity)
+    (void)it;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
 #if B2_PR_EPI_SUSPEND
       mbar_wait_suspend(&tfull[acc], aph);
@@ -389,6 +503,19 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
       tc_fence_after();
       uint32_t words[ECH];
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS + c0 * 32;
+      if constexpr (ECH <= 2) {
+        // every chunk's load in flight at once, one wait: the accumulator goes
+        // back to the MMA after a single TMEM round trip
+        uint32_t v[ECH][32];
+#pragma unroll
+        for (int c = 0; c < ECH; ++c) tmem_ld32(ta + c * 32, v[c]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+#pragma unroll
+        for (int c = 0; c < ECH; ++c) words[c] = thr_word<true>(v[c], sthr + (c0 + c) * 16);
+      } else {
       // software-pipelined: chunk c + 1 is in flight while chunk c is thresholded
       uint32_t va[32], vb[32];
       tmem_ld32(ta, va);
@@ -406,11 +533,41 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
       }
-      if (ECH < 2) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
+      if constexpr (ALIGN) {
+        const int64_t pix = t * BM + r;  // tiles cover whole images: every row is a pixel
+        if (!g.pool) {
+          uint32_t* o = g.out_bits + pix * g.ldo32;
+#pragma unroll
+          for (int c = 0; c < ECH; ++c)
+            if (c0 + c < g.ldo32) o[c0 + c] = words[c];
+        } else {
+          // 2x2/2 pool inside the tile: OR / AND of the horizontal pair by
+          // shuffle, then of the vertical pair (row r + W) through shared
+          // memory (double-buffered by tile parity: one barrier per tile)
+          uint2* sp = spool + (size_t)(it & 1) * BM * (BN / 32);
+#pragma unroll
+          for (int c = 0; c < ECH; ++c) {
+            const uint32_t w1 = __shfl_xor_sync(0xffffffffu, words[c], 1);
+            sp[(c0 + c) * BM + r] = make_uint2(words[c] | w1, words[c] & w1);  // [column word][row]: no bank conflicts
+          }
+          epi_bar<PR_NEPI>();
+          const int ty = r >> g.wshift, x = r & ((1 << g.wshift) - 1);
+          if (!(ty & 1) && !(x & 1)) {
+            const int64_t n = pix / g.HW;
+            const int y = (int)((pix - n * g.HW) >> g.wshift);
+            const int wp = (1 << g.wshift) >> 1;
+            uint32_t* o = g.out_bits + ((n * (g.H >> 1) + (y >> 1)) * wp + (x >> 1)) * g.ldo32;
+#pragma unroll
+            for (int c = 0; c < ECH; ++c) {
+              const uint2 a = sp[(c0 + c) * BM + r], b = sp[(c0 + c) * BM + r + (1 << g.wshift)];
+              const uint32_t gm = sgm[c0 + c];
+              if (c0 + c < g.ldo32) o[c0 + c] = ((a.x | b.x) & gm) | ((a.y & b.y) & ~gm);
+            }
+          }
+        }
+        ++it;
+      } else {
       const int64_t v = t * BM + r;
       if (v < g.Vtotal) {
         int64_t n;
@@ -422,6 +579,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT>()), 1)
           for (int c = 0; c < ECH; ++c)
             if (c0 + c < g.ldo32) o[c0 + c] = words[c];
         }
+      }
       }
       if (++acc == PR_ACC) acc = 0, aph ^= 1;
     }
@@ -460,9 +618,10 @@ __global__ void k_expand_f4_cells(const uint64_t* __restrict__ w, int64_t rows, 
 }
 
 template <int BNT>
-inline int padrow_smem_bytes(int nkb, int band_bytes) {
-  return nkb * BNT * 128 + pr_bands<BNT>() * band_bytes + BNT / 2 * 16 + BNT / 8 +
-         8 * (1 + 2 * pr_bands<BNT>() + 2 * pr_acc<BNT>()) + 16 + 8 * 128 + 1024;  // + MMA offset table (<= 128)
+inline int padrow_smem_bytes(int nkb, int band_bytes, int nbands = pr_bands<BNT>(), bool pool_buf = false) {
+  return nkb * BNT * 128 + nbands * band_bytes + BNT / 2 * 16 + BNT / 8 + 8 * (1 + 2 * PR_BANDS_MAX + 2 * pr_acc<BNT>()) +
+         16 + 8 * 128 +  // MMA offset table (<= 128)
+         (pool_buf ? 2 * BM * (BNT / 32) * 8 : 0) + 1024;
 }
 
 // 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for

@@ -166,11 +166,15 @@ class _ByteConvFused(_Stage):
         super().alloc(cap)
         h, w, c = self.in_shape
         r = self.rec
-        n = int(_lib.raw("b2_tc_byte_conv_scratch_bytes")(cap, h, w, c, r.kh, r.kw, r.stride, r.pad))
+        # the fused kernel (b2_tc_byte_conv_path == 1) needs no unrolled scratch
+        self.fused = self.tc and int(_lib.raw("b2_tc_byte_conv_path")(cap, h, w, c, r.filters, r.kh, r.kw, r.stride,
+                                                                         r.pad, 0)) == 1
+        n = 8 if self.fused else int(_lib.raw("b2_tc_byte_conv_scratch_bytes")(cap, h, w, c, r.kh, r.kw, r.stride,
+                                                                                 r.pad))
         self.codes = _dev.empty((n,), np.uint8) if self.tc else None
 
     def launches(self):
-        return 2 if self.tc else 1
+        return (1 if self.fused else 2) if self.tc else 1
 
     def launch(self, net, batch, st):
         h, w, c = self.in_shape

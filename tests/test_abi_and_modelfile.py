@@ -164,3 +164,30 @@ def test_model_size_paper_mlp():
 def test_work_per_image():
     assert 2 * zoo.macs_per_image(zoo.bcnn_spec()) == 1233932288
     assert 2 * zoo.macs_per_image(zoo.bmlp_spec()) == 118571008
+
+
+# (h, w, c, filters, pool, batch) -> fp4 conv kernel (b2_tc4_conv_path: 0 im2col,
+# 1 split-K, 2 padded-row, 3 row-aligned padded-row).  Pins which kernel each
+# GPU parity case of tests/test_gpu_tc.py exercises, and BCNN's layers at the
+# bench batch.  Path choice is host logic: it runs without a GPU.
+CONV_PATHS = [
+    ((32, 32, 128, 128, 1, 20), 3), ((16, 16, 128, 64, 0, 80), 3), ((16, 16, 128, 256, 0, 80), 3),
+    ((64, 64, 128, 128, 1, 6), 3), ((8, 16, 128, 96, 1, 160), 3), ((4, 32, 128, 128, 0, 160), 3),
+    ((8, 8, 128, 100, 1, 240), 0), ((16, 16, 128, 200, 1, 80), 0), ((62, 62, 128, 128, 0, 6), 2),
+    ((8, 190, 128, 64, 0, 20), 2), ((8, 191, 128, 64, 0, 20), 0), ((32, 32, 128, 128, 1, 2), 0),
+    ((16, 64, 128, 200, 1, 20), 0), ((4, 4, 512, 512, 1, 1), 1), ((8, 8, 512, 200, 0, 3), 1),
+    # BCNN conv2..conv6 at 8192 images
+    ((32, 32, 128, 128, 1, 8192), 3), ((16, 16, 128, 256, 0, 8192), 3), ((16, 16, 256, 256, 1, 8192), 0),
+    ((8, 8, 256, 512, 0, 8192), 0), ((8, 8, 512, 512, 1, 8192), 0),
+]
+
+
+@pytest.mark.parametrize("shape,path", CONV_PATHS)
+def test_conv_kernel_choice(shape, path):
+    h, w, c, f, pool, batch = shape
+    assert _lib._so.b2_tc4_conv_path(batch, h, w, c, f, 3, 3, 1, 1, pool) == path
+
+
+def test_padrow_rejects_inexact_index_split():
+    # a 4000 x 4000 1x1 conv would split virtual rows inexactly
+    assert _lib._so.b2_tc4_conv_path(1, 4000, 4000, 128, 128, 1, 1, 1, 0, 0) == 0

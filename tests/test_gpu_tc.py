@@ -98,7 +98,10 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
                                                 # warps cover (W = 190) and the first one past it (im2col kernel)
                                                 (62, 62, 128, 128, False, 6), (64, 64, 128, 128, True, 6),
                                                 (16, 64, 128, 200, True, 20), (8, 190, 128, 64, False, 20),
-                                                (8, 191, 128, 64, False, 20)])
+                                                (8, 191, 128, 64, False, 20),
+                                                # row-aligned padded-row tiles (pool fused): one image per tile
+                                                # at 8x16, four rows at 4x32
+                                                (8, 16, 128, 96, True, 160), (4, 32, 128, 128, False, 160)])
 def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch, fmt):
     rng = np.random.default_rng(5 + h + c + f)
     xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
@@ -421,3 +424,57 @@ def test_tc_conv_bn_pack_random_geometry(oracle, seed, fmt):
     _lib.call(_lib.tc_entry("conv_bn_pack", fmt), _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1,
               int(pool), th(cal), _dev.P(out), _dev.stream())
     assert np.array_equal(_dev.download(out, np.uint64), np.stack(want)), (h, w, c, f, pool, batch)
+
+
+# the fused first-layer kernel (tc_byteconv.cuh, b2_tc_byte_conv_path == 1):
+# row-aligned tiles, window + folded threshold in one int8 MMA; gamma = 0
+# (ALWAYS / NEVER sentinels) and gamma < 0 (le filters, negated weights) in
+# both batch norms; 128- and 256-column tiles
+@pytest.mark.parametrize("h,w,c,f,kh,batch", [(32, 32, 3, 128, 3, 3), (16, 16, 3, 64, 3, 5), (8, 16, 2, 200, 3, 4),
+                                              (32, 32, 1, 128, 5, 2), (64, 64, 3, 96, 3, 1), (16, 16, 1, 10, 3, 7),
+                                              (32, 32, 3, 256, 3, 2), (4, 32, 3, 128, 1, 3)])
+def test_fused_byte_conv_vs_oracle(oracle, h, w, c, f, kh, batch):
+    pad = (kh - 1) // 2
+    assert _lib._so.b2_tc_byte_conv_path(batch, h, w, c, f, kh, kh, 1, pad, 0) == 1
+    rng = np.random.default_rng(h * w * 7 + c + f + kh)
+    imgs = rng.integers(0, 256, (batch, h, w, c), dtype=np.uint8)
+    imgs[0, :2] = 0
+    imgs[-1, -2:] = 255
+    bn0 = rand_bn(rng, c, 100.0)
+    if c > 1:
+        bn0.gamma[1] *= -1
+    bn0 = BatchNormLayer(bn0.mean, bn0.var, bn0.gamma, bn0.beta)
+    k = kh * kh * c
+    wt = oracle.pack_lines(rand_pm1(rng, f, k))
+    bn1 = rand_bn(rng, f, 4.0)
+    bn1.gamma[::7] = 0.0
+    bn1.gamma[3::5] *= -1
+    bn1 = BatchNormLayer(bn1.mean, bn1.var, bn1.gamma, bn1.beta)
+    corr = oracle.compute_correction(wt, (h, w, c), (kh, kh), 1, pad)
+    want = []
+    for i in range(batch):
+        if c == 1:
+            lines = oracle.threshold_sign_pack(imgs[i].reshape(h, w).astype(np.int64), np.repeat(bn0.thresh, w),
+                                               np.repeat(bn0.ge_dir, w), False)
+        else:
+            lines = oracle.threshold_sign_pack(imgs[i].reshape(h * w, c).astype(np.int64), bn0.thresh, bn0.ge_dir,
+                                               False)
+        acc = oracle.bgemm(oracle.unroll_packed(lines, h, w, c, kh, kh, 1, pad), wt, k) + corr
+        want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn1.thresh, bn1.ge_dir, False))
+    cal0 = layers.calibrate_device(bn0.mean, bn0.var, bn0.gamma, bn0.beta, bn0.eps, 255)
+    cal1 = layers.calibrate_device(bn1.mean, bn1.var, bn1.gamma, bn1.beta, bn1.eps, k)
+    w8 = _dev.tc_weights(_dev.upload(wt), f, k, "i8")
+    out = _dev.empty((batch, h * w, -(-f // 64)), np.uint64)
+    out.fill_(-1)  # every word must be written
+    codes = _dev.empty((8,), np.uint8)  # the fused kernel takes no scratch
+    c0 = _lib.launch_count()
+    _lib.call("b2_tc_byte_conv_bn_pack", _dev.P(_dev.upload(imgs)), batch, h, w, c, th(cal0), _dev.P(w8), f, kh, kh,
+              1, pad, 0, th(cal1), _dev.P(codes), _dev.P(out), _dev.stream())
+    assert _lib.launch_count() - c0 == 1
+    assert np.array_equal(_dev.download(out, np.uint64), np.stack(want))
+
+
+@pytest.mark.parametrize("h,w,c,f,kh,pad,stride,pool", [(16, 12, 3, 64, 3, 1, 1, True), (9, 9, 4, 200, 5, 2, 2, False),
+                                                        (8, 8, 8, 32, 3, 1, 1, True), (5, 7, 1, 10, 3, 0, 1, False)])
+def test_byte_conv_unfused_path_kept(h, w, c, f, kh, pad, stride, pool):
+    assert _lib._so.b2_tc_byte_conv_path(3, h, w, c, f, kh, kh, stride, pad, int(pool)) == 0
