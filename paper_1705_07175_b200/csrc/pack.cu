@@ -112,6 +112,164 @@ __global__ void __launch_bounds__(256) k_pack_byte_planes(const uint8_t* __restr
   }
 }
 
+// ---------------------------------------------------------------- TMA-fed variants
+// Both packing kernels are HBM streams; with the bytes in flight held in
+// registers their occupancy (and so the bytes in flight) is register-bound.
+// These variants stage each warp's input through a 3-slot shared-memory ring
+// filled by 1-D bulk copies (cp.async.bulk, completion on an mbarrier): the
+// copies of the next two chunks are in flight while the warp packs the
+// current one from shared memory.  Eligible when every chunk is a 16-byte
+// multiple at a 16-byte aligned address (lines of bits % 4 == 0 floats /
+// bits % 16 == 0 bytes); other shapes keep the kernels above.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done)
+                 : "r"(smem_addr(bar)), "r"(parity)
+                 : "memory");
+  } while (!done);
+}
+
+constexpr int PK_WARPS = 8, PK_SLOTS = 3;
+
+// chunk = 1024 floats (32 words) of one line, as k_pack_lines_f32
+__global__ void __launch_bounds__(32 * PK_WARPS) k_pack_lines_f32_tma(const float* __restrict__ lines, int64_t n_lines,
+                                                                       int64_t bits, int64_t wpl32,
+                                                                       uint32_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t pk_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* ring = reinterpret_cast<float*>(pk_smem) + warp * PK_SLOTS * 1024;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pk_smem + PK_WARPS * PK_SLOTS * 4096) + warp * PK_SLOTS;
+  if (lane == 0)
+    for (int i = 0; i < PK_SLOTS; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[i])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  pdl_entry();
+  const uint32_t cpl = (uint32_t)((wpl32 + 31) / 32);  // chunks per line
+  const uint32_t chunks = (uint32_t)(n_lines * cpl);
+  const uint32_t step = gridDim.x * PK_WARPS;
+  const uint32_t c0 = blockIdx.x * PK_WARPS + warp;
+  auto issue = [&](uint32_t c, int slot) {
+    if (c >= chunks) return;
+    const uint32_t line = c / cpl, j = c - line * cpl;
+    const int64_t e0 = (int64_t)j * 1024;
+    const int64_t n = bits - e0 < 1024 ? bits - e0 : 1024;
+    bulk_g2s(ring + slot * 1024, lines + line * bits + e0, (uint32_t)(n * 4), &bars[slot]);
+  };
+  if (lane == 0) {
+    issue(c0, 0);
+    issue(c0 + step, 1);
+  }
+  int slot = 0;
+  uint32_t ph = 0;
+  for (uint32_t c = c0; c < chunks; c += step) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of that slot came first
+      issue(c + 2 * step, slot == 0 ? PK_SLOTS - 1 : slot - 1);
+    }
+    const uint32_t line = c / cpl, j = c - line * cpl;
+    const int64_t e0 = (int64_t)j * 1024;
+    const int n = (int)(bits - e0 < 1024 ? bits - e0 : 1024);
+    bar_wait(&bars[slot], ph);
+    const float* v = ring + slot * 1024;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int e = r * 32 + lane;
+      const uint32_t w = __ballot_sync(0xffffffffu, e < n && !(v[e] < 0.0f));
+      if (lane == r) mine = w;
+    }
+    if (j * 32 + lane < wpl32) out[line * wpl32 + j * 32 + lane] = mine;
+    __syncwarp();
+    if (++slot == PK_SLOTS) slot = 0, ph ^= 1;
+  }
+}
+
+// 8x8 bit transpose of a 64-bit word (row i = byte i): byte p of the result
+// holds bit p of every input byte (Hacker's Delight delta swaps)
+__device__ __forceinline__ uint64_t transpose8(uint64_t x) {
+  uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+  x = x ^ t ^ (t << 7);
+  t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+  x = x ^ t ^ (t << 14);
+  t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+  return x ^ t ^ (t << 28);
+}
+
+// chunk = LB whole lines (LB = 4096 / bits, lines of at most 4096 bytes): one
+// bulk copy per chunk (small copies are TMA-issue-bound), then per line and
+// 512-byte segment lane l packs bytes [16 l, 16 l + 16) by two 8x8 bit
+// transposes; even lanes join their odd neighbour's 16 bits into the word
+constexpr int PK_BYTES_SLOT = 4096;
+__global__ void __launch_bounds__(32 * PK_WARPS) k_pack_byte_planes_tma(const uint8_t* __restrict__ lines,
+                                                                         int64_t n_lines, int64_t bits, int64_t wpl32,
+                                                                         uint32_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t pk_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = pk_smem + warp * PK_SLOTS * PK_BYTES_SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pk_smem + PK_WARPS * PK_SLOTS * PK_BYTES_SLOT) + warp * PK_SLOTS;
+  if (lane == 0)
+    for (int i = 0; i < PK_SLOTS; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[i])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  pdl_entry();
+  const int lb = (int)(PK_BYTES_SLOT / bits);  // lines per chunk
+  const int bw = (int)bits;
+  const uint32_t chunks = (uint32_t)((n_lines + lb - 1) / lb);
+  const uint32_t step = gridDim.x * PK_WARPS;
+  const uint32_t c0 = blockIdx.x * PK_WARPS + warp;
+  auto issue = [&](uint32_t c, int slot) {
+    if (c >= chunks) return;
+    const int64_t l0 = (int64_t)c * lb;
+    const int64_t nl = n_lines - l0 < lb ? n_lines - l0 : lb;
+    bulk_g2s(ring + slot * PK_BYTES_SLOT, lines + l0 * bits, (uint32_t)(nl * bits), &bars[slot]);
+  };
+  if (lane == 0) {
+    issue(c0, 0);
+    issue(c0 + step, 1);
+  }
+  int slot = 0;
+  uint32_t ph = 0;
+  for (uint32_t c = c0; c < chunks; c += step) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of that slot came first
+      issue(c + 2 * step, slot == 0 ? PK_SLOTS - 1 : slot - 1);
+    }
+    const int64_t l0 = (int64_t)c * lb;
+    const int nl = (int)(n_lines - l0 < lb ? n_lines - l0 : lb);
+    bar_wait(&bars[slot], ph);
+    const uint8_t* buf = ring + slot * PK_BYTES_SLOT;
+    for (int li = 0; li < nl; ++li) {
+      const int64_t line = l0 + li;
+      for (int b0 = 0; b0 < bw; b0 += 512) {
+        const int n = bw - b0 < 512 ? bw - b0 : 512;  // valid bytes of this segment
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (16 * lane < n) x = *reinterpret_cast<const uint4*>(buf + li * bw + b0 + 16 * lane);  // n % 16 == 0
+        const uint64_t t0 = transpose8(((uint64_t)x.y << 32) | x.x), t1 = transpose8(((uint64_t)x.w << 32) | x.z);
+        const int64_t w = b0 / 32 + (lane >> 1);
+        uint32_t* o = out + line * wpl32 + w;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const uint32_t m16 = (uint32_t)((t0 >> (8 * p)) & 0xFF) | ((uint32_t)((t1 >> (8 * p)) & 0xFF) << 8);
+          const uint32_t hi = __shfl_down_sync(0xffffffffu, m16, 1);
+          if (!(lane & 1) && w < wpl32) o[(int64_t)p * n_lines * wpl32] = m16 | (hi << 16);
+        }
+      }
+    }
+    __syncwarp();
+    if (++slot == PK_SLOTS) slot = 0, ph ^= 1;
+  }
+}
+
 }  // namespace b2
 
 using namespace b2;
@@ -131,6 +289,15 @@ int b2_pack_lines_f32(const float* lines, int64_t n_lines, int64_t bits, uint64_
   int64_t wpl32 = 2 * wpl64(bits);
   int64_t chunks = n_lines * cdiv(wpl32, 32);
   if (!chunks) return 0;
+  if (bits % 4 == 0 && (reinterpret_cast<uintptr_t>(lines) & 15) == 0 && chunks < (int64_t)1 << 31) {
+    static std::atomic<uint64_t> attr{0};
+    const int smem = PK_WARPS * PK_SLOTS * (4096 + 8);
+    smem_optin(k_pack_lines_f32_tma, smem, attr);
+    const int64_t blocks = cdiv(chunks, PK_WARPS) < 148 * 2 ? cdiv(chunks, PK_WARPS) : 148 * 2;
+    launch_k(k_pack_lines_f32_tma, (unsigned)blocks, 32 * PK_WARPS, smem, S(stream), lines, n_lines, bits, wpl32,
+             (uint32_t*)out);
+    return launched();
+  }
   const int64_t blocks = cdiv(chunks, 8) < 148 * 32 ? cdiv(chunks, 8) : 148 * 32;  // grid-stride beyond
   launch_k(k_pack_lines_f32, (unsigned)blocks, 256, 0, S(stream), lines, n_lines, bits, wpl32, (uint32_t*)out);
   return launched();
@@ -150,6 +317,17 @@ int b2_pack_byte_planes(const uint8_t* lines, int64_t n_lines, int64_t bits, uin
   int64_t wpl32 = 2 * wpl64(bits);
   int64_t chunks = n_lines * cdiv(wpl32, 16);
   if (!chunks) return 0;
+  if (bits % 16 == 0 && bits <= PK_BYTES_SLOT && (reinterpret_cast<uintptr_t>(lines) & 15) == 0 &&
+      n_lines < (int64_t)1 << 31) {
+    static std::atomic<uint64_t> attr{0};
+    const int smem = PK_WARPS * PK_SLOTS * (PK_BYTES_SLOT + 8);
+    smem_optin(k_pack_byte_planes_tma, smem, attr);
+    const int64_t tchunks = cdiv(n_lines, PK_BYTES_SLOT / bits);
+    const int64_t blocks = cdiv(tchunks, PK_WARPS) < 148 * 2 ? cdiv(tchunks, PK_WARPS) : 148 * 2;
+    launch_k(k_pack_byte_planes_tma, (unsigned)blocks, 32 * PK_WARPS, smem, S(stream), lines, n_lines, bits, wpl32,
+             (uint32_t*)out);
+    return launched();
+  }
   const int64_t blocks = cdiv(chunks, 8) < 148 * 32 ? cdiv(chunks, 8) : 148 * 32;  // grid-stride beyond
   launch_k(k_pack_byte_planes, (unsigned)blocks, 256, 0, S(stream), lines, n_lines, bits, wpl32, (uint32_t*)out);
   return launched();

@@ -1291,16 +1291,28 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       tc_fence_after();
       uint32_t words[ECH];
       const int4* trow = sthr + ((tcol + ec0) >> 1);  // (mul, add) pairs of this warp's columns
-      // TMEM -> registers, software-pipelined: chunk c + 1 is in flight while
-      // chunk c is thresholded (tcgen05.wait::ld waits for all prior loads)
+      // TMEM -> registers.  Up to two chunks per warp: both loads in flight,
+      // one wait, the accumulator goes back to the MMA before any math (the
+      // single 256-column accumulator's drain is on the MMA's critical path);
+      // more chunks: software-pipelined, chunk c + 1 in flight while chunk c
+      // is processed (tcgen05.wait::ld waits for all prior loads)
+      constexpr bool ALL_AT_ONCE = ECH <= 2;
       uint32_t va[32], vb[32];
       tmem_ld32(tmem + lane_addr + acc * ACC_COLS, va);
-      tmem_wait_ld();
+      if constexpr (ALL_AT_ONCE) {
+        if (ECH == 2) tmem_ld32(tmem + lane_addr + acc * ACC_COLS + 32, vb);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {
+        tmem_wait_ld();
+      }
 #pragma unroll
       for (int c = 0; c < ECH; ++c) {
         uint32_t(&v)[32] = (c & 1) ? vb : va;
         uint32_t(&vn)[32] = (c & 1) ? va : vb;
-        if (c + 1 < ECH) tmem_ld32(tmem + lane_addr + acc * ACC_COLS + (c + 1) * 32, vn);
+        if (!ALL_AT_ONCE && c + 1 < ECH) tmem_ld32(tmem + lane_addr + acc * ACC_COLS + (c + 1) * 32, vn);
         const int nb = n0 + ec0 + c * 32;
         if constexpr (EM == E_AFFINE) {
           // _kernels.py:285-295 bn_affine: three separately rounded IEEE
@@ -1334,16 +1346,16 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           if constexpr (EM == E_POOLPACK) w = pool_word(w, sgm[((tcol + ec0) >> 5) + c]);
           words[c] = w;
         }
-        if (c + 1 < ECH) tmem_wait_ld();
+        if (!ALL_AT_ONCE && c + 1 < ECH) tmem_wait_ld();
 #if B2_EARLY_RELEASE
-        if (c + 2 == ECH) {  // every chunk is in registers: hand the accumulator back before the last one's math
+        if (!ALL_AT_ONCE && c + 2 == ECH) {  // every chunk is in registers: hand the accumulator back before the last one's math
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
 #endif
       }
-      if (!B2_EARLY_RELEASE || ECH < 2) {
+      if (!ALL_AT_ONCE && !B2_EARLY_RELEASE) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);

@@ -12,6 +12,9 @@ Writes into tests/golden/:
   * networks.npz            — scores of the fixture models and of the
                               BASELINE-sized BMLP / BCNN on seeded images,
                               plus the SHA-256 of each model's serialized bytes
+  * vgg.bdnn, acceptance.npz — the reference's acceptance CNN and its
+                              1000-image scores (both backends), and 1024
+                              seeded images each through BCNN / BMLP
 
 The BASELINE-sized models are built here with the reference's record
 classes using the recipe documented in paper_1705_07175_b200/zoo.py
@@ -214,8 +217,51 @@ def network_vectors():
     return out
 
 
+def vgg_like_cnn(rng):
+    """The reference acceptance network (pkg/tests/test_acceptance.py:80-98):
+    32x32x3 input, 2x(32C3) - MP2 - 2x(64C3) - MP2 - FC256 - FC10, drawn from
+    `rng` in the same call order."""
+    return ModelSpec((32, 32, 3), [
+        bn(rng, 3, 100.0),
+        ConvRecord(32, 3, 3, 1, 1, 3, pack_rows(rng, 32, 27)), bn(rng, 32, 8.0),
+        ConvRecord(32, 3, 3, 1, 1, 32, pack_rows(rng, 32, 288)), MaxPoolRecord(2, 2, 2), bn(rng, 32, 30.0),
+        ConvRecord(64, 3, 3, 1, 1, 32, pack_rows(rng, 64, 288)), bn(rng, 64, 30.0),
+        ConvRecord(64, 3, 3, 1, 1, 64, pack_rows(rng, 64, 576)), MaxPoolRecord(2, 2, 2), bn(rng, 64, 60.0),
+        DenseRecord(256, 4096, pack_rows(rng, 256, 4096)), bn(rng, 256, 20.0),
+        DenseRecord(10, 256, pack_rows(rng, 10, 256)), bn(rng, 10, 4.0),
+    ])
+
+
+def acceptance_vectors():
+    """Wider parity set (round 2): the reference's own acceptance network with
+    its 1000-image cross-backend check (test_acceptance.py:166-179), both
+    backends' scores, and 1024 distinct images each for the BASELINE-sized
+    BCNN and BMLP.  Images are NOT stored: tests regenerate them from the
+    seeds below (same rng recipe), so the fixture stays small."""
+    from bitnn.network import Backend
+    out = {}
+    rng = np.random.default_rng(2028)
+    spec = vgg_like_cnn(rng)
+    with open(os.path.join(HERE, "vgg.bdnn"), "wb") as fh:
+        fh.write(write_model(spec))
+    packed, ref = Network(spec, Backend.PACKED), Network(spec, Backend.REFERENCE)
+    sp, sr = [], []
+    for _ in range(1000):
+        img = rng.integers(0, 256, (32, 32, 3), dtype=np.uint8)
+        sp.append(forward(packed, img).copy())
+        sr.append(forward(ref, img).copy())
+    out["vgg_packed_scores"], out["vgg_reference_scores"] = np.stack(sp), np.stack(sr)
+    for name, spec, shape in (("bcnn", bcnn_spec(), (32, 32, 3)), ("bmlp", bmlp_spec(), (784,))):
+        net = Network(spec)
+        imgs = np.random.default_rng(4242).integers(0, 256, (1024,) + shape, dtype=np.uint8)
+        out[f"{name}1024_scores"] = np.stack([forward(net, im).copy() for im in imgs])
+    out["seeds"] = np.array([2028, 4242])
+    return out
+
+
 if __name__ == "__main__":
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernel_vectors())
     np.savez_compressed(os.path.join(HERE, "networks.npz"), **network_vectors())
+    np.savez_compressed(os.path.join(HERE, "acceptance.npz"), **acceptance_vectors())
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -231,3 +231,28 @@ def test_dense_bn_pack_batched_vs_oracle(oracle):
         _lib.call("b2_dense_bn_pack", _dev.P(_dev.upload(x)), batch, _dev.P(_dev.upload(wt)), units, -(-k // 64), k,
                   layers._thresh_struct(cal["thresh32"], cal["thresh64"], cal["ge"]), _dev.P(out), _dev.stream())
         assert np.array_equal(_dev.download(out, np.uint64), want), (batch, units, k)
+
+
+# the TMA-fed packing kernels (bits % 4 == 0 floats, bits % 16 == 0 bytes):
+# whole and partial 1024-float / 512-byte chunks, more chunks than warps in
+# flight, NaN / -0.0 / +-inf, against the oracle
+@pytest.mark.parametrize("lines,bits", [(1, 4), (3, 1028), (7, 4096), (5, 12), (600, 1024), (2, 8192), (9000, 64)])
+def test_pack_lines_tma_vs_oracle(oracle, lines, bits):
+    rng = np.random.default_rng(lines * 7 + bits)
+    x = rng.standard_normal((lines, bits)).astype(np.float32)
+    x.flat[::97] = 0.0
+    x.flat[5::101] = -0.0
+    x.flat[7::103] = np.nan
+    x.flat[9::107] = -np.inf
+    assert np.array_equal(tensor.pack_lines(x), oracle.pack_lines(x))
+
+
+@pytest.mark.parametrize("lines,bits", [(5, 16), (3, 784), (4, 512), (2, 528), (3000, 784), (7, 1024)])
+def test_byte_planes_tma_vs_oracle(oracle, lines, bits):
+    rng = np.random.default_rng(lines + bits)
+    u = rng.integers(0, 256, (lines, bits), dtype=np.uint8)
+    wpl = -(-bits // 64)
+    out = _dev.empty((8, lines, wpl), np.uint64)
+    out.fill_(-1)
+    _lib.call("b2_pack_byte_planes", _dev.P(_dev.upload(u)), lines, bits, _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), oracle.pack_byte_planes(u))

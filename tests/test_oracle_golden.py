@@ -109,3 +109,24 @@ def test_baseline_models_scores(networks_golden, oracle):
         want = networks_golden[f"{name}_scores"][:n]
         for i in range(n):
             assert np.array_equal(net.forward(imgs[i]), want[i]), (name, i)
+
+
+def test_acceptance_set_oracle(oracle):
+    """The oracle against the reference's acceptance CNN (1000 images, both
+    backends agree: argmax identical, gap < 1e-4) and 1024 distinct images
+    through the BASELINE BMLP / a 96-image sample through BCNN."""
+    from acceptance_set import images1024, vgg_set
+    acc = np.load(os.path.join(GOLDEN, "acceptance.npz"))
+    spec, imgs = vgg_set()
+    net = oracle.OracleNetwork(spec)
+    got = np.stack([net.forward(im) for im in imgs])
+    assert np.array_equal(got, acc["vgg_packed_scores"])
+    assert np.array_equal(np.argmax(got, 1), np.argmax(acc["vgg_reference_scores"], 1))
+    assert float(np.max(np.abs(got - acc["vgg_reference_scores"]))) < 1e-4
+    bm = oracle.OracleNetwork(zoo.bmlp_spec())
+    x = images1024("bmlp")
+    assert np.array_equal(np.stack([bm.forward(im) for im in x]), acc["bmlp1024_scores"])
+    bc = oracle.OracleNetwork(zoo.bcnn_spec())
+    x = images1024("bcnn")
+    idx = np.arange(0, 1024, 11)
+    assert np.array_equal(np.stack([bc.forward(x[i]) for i in idx]), acc["bcnn1024_scores"][idx])
