@@ -10,6 +10,7 @@
 #include "tc_i8.cuh"
 #include "tc_padrow.cuh"
 #include "tc_byteconv.cuh"
+#include "tc_pair.cuh"
 
 #ifndef B2_RESIDENT_B
 #define B2_RESIDENT_B 1
@@ -270,6 +271,36 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   return launched();
 }
 
+// CTA-pair kernel (tc_pair.cuh): 256 x 256 tiles over two SMs, a third less
+// shared-memory traffic per MAC than the single-CTA 128 x 256 tile.
+#ifndef B2_PAIR
+#define B2_PAIR 0  // measured slower than the single-CTA kernel; B2_PAIR=1 opts in
+#endif
+inline bool pair_on() {
+  static const int on = [] {
+    const char* e = getenv("B2_PAIR");
+    return e ? atoi(e) : B2_PAIR;
+  }();
+  return on != 0;
+}
+template <int AM, int EM>
+int launch_pair(Args g, const int8_t* b, int64_t kpad, int64_t k, cudaStream_t st) {
+  g.nkb = (int)((k + PAIR_BKS - 1) / PAIR_BKS);
+  g.klast = (int)(((k - 1) % PAIR_BKS) / 64 + 1);
+  g.resb = 0;
+  g.ksplit = 1;
+  CUtensorMap map;
+  if (int rc = make_bmap(&map, b, g.N, kpad / 2, PAIR_BN / 2)) return rc;
+  auto kern = k_pair_gemm<AM, EM>;
+  constexpr int smem = pair_smem_bytes();
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(kern, smem, attr);
+  const int64_t tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + PAIR_BN - 1) / PAIR_BN);
+  const int64_t pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  launch_kc(2, kern, (unsigned)(2 * pairs), 32 * (4 + PAIR_NPW + PAIR_NEPI), smem, st, map, g);
+  return launched();
+}
+
 // Split-K for launches with few tiles (small batches) and deep K: the ks K
 // splits of each 128x128 tile run as one cluster and reduce over distributed
 // shared memory, so the serial K walk of a deep layer spreads over ks SMs.
@@ -334,6 +365,11 @@ int launch_f4(Args g, const int8_t* b, int64_t kpad, cudaStream_t st, int64_t k)
         const int64_t tiles256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
         if (B2_SMALLM_TILES && tiles256 < B2_SMALLM_TILES)
           return launch_bn<128, AM, EM, 8, 512, 4, false, true>(g, b, kpad, k, st);
+        // enough 256 x 256 tiles for every SM pair: the CTA-pair kernel
+        if constexpr (AM == A_ROWS || AM == A_CONV) {
+          if (pair_on() && ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 255) / 256) >= num_sms() / 2)
+            return launch_pair<AM, EM>(g, b, kpad, k, st);
+        }
         return launch_bn<256, AM, EM, 8, 256, B2_NEPI_F4_256, false, true>(g, b, kpad, k, st);
       }
       if constexpr (AM == A_ROWS) return launch_bn<128, AM, EM, 8, 512, B2_NEPI_F4_128, false, true>(g, b, kpad, k, st);

@@ -478,3 +478,88 @@ def test_fused_byte_conv_vs_oracle(oracle, h, w, c, f, kh, batch):
                                                         (8, 8, 8, 32, 3, 1, 1, True), (5, 7, 1, 10, 3, 0, 1, False)])
 def test_byte_conv_unfused_path_kept(h, w, c, f, kh, pad, stride, pool):
     assert _lib._so.b2_tc_byte_conv_path(3, h, w, c, f, kh, kh, stride, pad, int(pool)) == 0
+
+
+# ---- CTA-pair kernel (tc_pair.cuh): launches with >= 74 256x256 tiles.
+# Ragged M / N / K, int32 / packed / pooled / float64 epilogues; the oracle
+# checks a sample of rows (every row of the GPU output is computed).
+def _sample_rows(m, n=48):
+    return np.unique(np.concatenate([np.arange(min(m, 8)), np.linspace(0, m - 1, n).astype(np.int64),
+                                     np.arange(max(0, m - 8), m)]))
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 1280, 1000), (19000, 300, 777), (9100, 2048, 4608), (38000, 257, 64)])
+def test_pair_bgemm_vs_oracle(oracle, m, n, k):
+    rng = np.random.default_rng(m + n + k)
+    a = zoo.pack_bits_host(rng.random((m, k)) >= 0.5)
+    b = zoo.pack_bits_host(rng.random((n, k)) >= 0.5)
+    got = _dev.download(gemm.bgemm_device(_dev.upload(a), m, _dev.upload(b), n, a.shape[1], k, engine="tc", fmt="f4"),
+                        np.int32)
+    rows = _sample_rows(m)
+    assert np.array_equal(got[rows], oracle.bgemm(np.ascontiguousarray(a[rows]), b, k))
+
+
+@pytest.mark.parametrize("batch,units,k", [(20000, 512, 2048), (40000, 300, 1000), (19000, 1024, 8192)])
+def test_pair_dense_bn_pack_vs_oracle(oracle, batch, units, k):
+    rng = np.random.default_rng(batch + units + k)
+    x = zoo.pack_bits_host(rng.random((batch, k)) >= 0.5)
+    wt = zoo.pack_bits_host(rng.random((units, k)) >= 0.5)
+    bn = rand_bn(rng, units, 30.0)
+    bn.gamma[::9] = 0.0
+    bn.gamma[4::7] *= -1
+    bn = BatchNormLayer(bn.mean, bn.var, bn.gamma, bn.beta)
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, k)
+    w8 = _dev.tc_weights(_dev.upload(wt), units, k, "f4")
+    out = _dev.empty((batch, -(-units // 64)), np.uint64)
+    _lib.call("b2_tc4_dense_bn_pack", _dev.P(_dev.upload(x)), batch, _dev.P(w8), units, -(-k // 64), k, th(cal),
+              _dev.P(out), _dev.stream())
+    got = _dev.download(out, np.uint64)
+    rows = _sample_rows(batch)
+    acc = oracle.bgemm(np.ascontiguousarray(x[rows]), wt, k)
+    want = np.stack([oracle.threshold_sign_pack(acc[i].reshape(1, -1), bn.thresh, bn.ge_dir, True)[0]
+                     for i in range(len(rows))])
+    assert np.array_equal(got[rows], want)
+
+
+@pytest.mark.parametrize("h,w,c,f,pool,batch", [(16, 16, 256, 256, True, 300), (8, 8, 512, 320, False, 1200),
+                                                (8, 8, 256, 512, True, 1200), (4, 4, 512, 512, False, 5000)])
+def test_pair_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch):
+    rng = np.random.default_rng(h + c + f + batch)
+    xs = zoo.pack_bits_host(rng.random((batch * h * w, c)) >= 0.5).reshape(batch, h * w, -1)
+    wt = zoo.pack_bits_host(rng.random((f, 9 * c)) >= 0.5)
+    bn = rand_bn(rng, f, 20.0)
+    bn.gamma[::7] = 0.0
+    bn.gamma[3::11] *= -1
+    bn = BatchNormLayer(bn.mean, bn.var, bn.gamma, bn.beta)
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 9 * c)
+    w8 = _dev.tc_weights(_dev.upload(wt), f, 9 * c, "f4")
+    sites = h * w // (4 if pool else 1)
+    out = _dev.empty((batch, sites, -(-f // 64)), np.uint64)
+    _lib.call("b2_tc4_conv_bn_pack", _dev.P(_dev.upload(xs)), batch, h, w, c, _dev.P(w8), f, 3, 3, 1, 1, int(pool),
+              th(cal), _dev.P(out), _dev.stream())
+    got = _dev.download(out, np.uint64)
+    corr = oracle.compute_correction(wt, (h, w, c), (3, 3), 1, 1)
+    for i in (0, 1, batch // 2, batch - 1):
+        acc = (oracle.bgemm(oracle.unroll_packed(xs[i], h, w, c, 3, 3, 1, 1), wt, 9 * c) + corr).reshape(h, w, f)
+        if pool:
+            acc = oracle.maxpool(acc, 2, 2, 2)
+        want = oracle.threshold_sign_pack(acc.reshape(-1, f), bn.thresh, bn.ge_dir, False)
+        assert np.array_equal(got[i], want), i
+
+
+def test_pair_dense_affine_vs_oracle(oracle):
+    batch, units, k = 20000, 300, 1000
+    rng = np.random.default_rng(3)
+    x = zoo.pack_bits_host(rng.random((batch, k)) >= 0.5)
+    wt = zoo.pack_bits_host(rng.random((units, k)) >= 0.5)
+    bn = rand_bn(rng, units, 10.0)
+    w8 = _dev.tc_weights(_dev.upload(wt), units, k, "f4")
+    out = _dev.empty((batch, units), np.float64)
+    mean, scale, beta = (_dev.upload(np.asarray(v, dtype=np.float64)) for v in (bn.mean64, bn.scale64, bn.beta64))
+    _lib.call("b2_tc4_dense_affine_f64", _dev.P(_dev.upload(x)), batch, _dev.P(w8), units, -(-k // 64), k,
+              _dev.P(mean), _dev.P(scale), _dev.P(beta), _dev.P(out), _dev.stream())
+    got = _dev.download(out, np.float64)
+    rows = _sample_rows(batch)
+    acc = oracle.bgemm(np.ascontiguousarray(x[rows]), wt, k)
+    want = np.stack([oracle.bn_affine(acc[i], bn.mean64, bn.scale64, bn.beta64) for i in range(len(rows))])
+    assert np.array_equal(got[rows], want)
