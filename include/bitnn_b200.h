@@ -315,6 +315,9 @@ int b2_tc4_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int 
  * layout of b2_expand_f4_cells: rows of b2_f4_cells_row_bytes(kh * kw)
  * bytes (per cell 64 e2m1 elements, the cell's c channel bits then zeros).
  * Pooled calls take a stream-ordered scratch like b2_tc4_conv_bn_pack.
+ * Also B2_EINVAL: a tile's band over 512 rows (w > 190 for 3x3: the
+ * producer warps cover one band row per thread) and weights plus the band
+ * ring over 227 KB of shared memory (e.g. any 7x7 window: 13 weight atoms).
  * Measured on BCNN conv1 (3 channels): 0.60 ms vs 0.36 ms for
  * b2_tc_byte_conv_bn_pack (nine K=64 MMAs per tile with 3 useful elements
  * each), so the network keeps the unrolled path; this entry is an opt-in

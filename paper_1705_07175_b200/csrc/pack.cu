@@ -194,6 +194,23 @@ __global__ void __launch_bounds__(32 * PK_WARPS) k_pack_lines_f32_tma(const floa
   }
 }
 
+// The same transpose on the word's two 32-bit halves (lo = bytes 0-3): the
+// 7- and 14-bit delta swaps stay inside a half, the 28-bit one swaps nibbles
+// between the halves
+__device__ __forceinline__ void transpose8_32(uint32_t& lo, uint32_t& hi) {
+  uint32_t t = (lo ^ (lo >> 7)) & 0x00AA00AAu;
+  lo ^= t ^ (t << 7);
+  t = (hi ^ (hi >> 7)) & 0x00AA00AAu;
+  hi ^= t ^ (t << 7);
+  t = (lo ^ (lo >> 14)) & 0x0000CCCCu;
+  lo ^= t ^ (t << 14);
+  t = (hi ^ (hi >> 14)) & 0x0000CCCCu;
+  hi ^= t ^ (t << 14);
+  t = (lo ^ (hi << 4)) & 0xF0F0F0F0u;
+  lo ^= t;
+  hi ^= t >> 4;
+}
+
 // 8x8 bit transpose of a 64-bit word (row i = byte i): byte p of the result
 // holds bit p of every input byte (Hacker's Delight delta swaps)
 __device__ __forceinline__ uint64_t transpose8(uint64_t x) {
@@ -254,14 +271,19 @@ __global__ void __launch_bounds__(32 * PK_WARPS) k_pack_byte_planes_tma(const ui
         const int n = bw - b0 < 512 ? bw - b0 : 512;  // valid bytes of this segment
         uint4 x = make_uint4(0, 0, 0, 0);
         if (16 * lane < n) x = *reinterpret_cast<const uint4*>(buf + li * bw + b0 + 16 * lane);  // n % 16 == 0
-        const uint64_t t0 = transpose8(((uint64_t)x.y << 32) | x.x), t1 = transpose8(((uint64_t)x.w << 32) | x.z);
+        transpose8_32(x.x, x.y);
+        transpose8_32(x.z, x.w);
         const int64_t w = b0 / 32 + (lane >> 1);
         uint32_t* o = out + line * wpl32 + w;
+        const int64_t pstride = n_lines * wpl32;
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
-          const uint32_t m16 = (uint32_t)((t0 >> (8 * p)) & 0xFF) | ((uint32_t)((t1 >> (8 * p)) & 0xFF) << 8);
+          // [byte p of bytes 0-7, byte p of bytes 8-15] of this lane, then the
+          // odd neighbour's two bytes above them: the plane's 32-bit word
+          const uint32_t a = p < 4 ? x.x : x.y, b = p < 4 ? x.z : x.w;
+          const uint32_t m16 = __byte_perm(a, b, (uint32_t)((p & 3) | ((4 + (p & 3)) << 4)));
           const uint32_t hi = __shfl_down_sync(0xffffffffu, m16, 1);
-          if (!(lane & 1) && w < wpl32) o[(int64_t)p * n_lines * wpl32] = m16 | (hi << 16);
+          if (!(lane & 1) && w < wpl32) o[p * pstride] = __byte_perm(m16, hi, 0x5410);
         }
       }
     }

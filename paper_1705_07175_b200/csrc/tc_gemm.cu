@@ -494,32 +494,35 @@ inline bool padrow_exact(const PadArgs& p) {
          (uint64_t)p.VI * (uint64_t)p.Wp < ((uint64_t)1 << 32);
 }
 
-inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t batch) {
+// Virtual-grid padded-row plan (packed-bit input): fills p with the
+// geometry, band and weight shapes the launch uses and returns false when the
+// layer does not qualify.  The path query (conv_path_f4) and the launch
+// (padrow_launch -> padrow_run) both go through it, so eligibility and launch
+// shape cannot drift apart.
+inline bool padrow_plan(const Args& g, int c, int64_t filters, int64_t k, int64_t batch, PadArgs& p) {
   static const int on = [] {
     const char* e = getenv("B2_PADROW");
     return e ? atoi(e) : B2_PADROW;
   }();
-  // the tile's input band (BM virtual rows plus the window's reach above and
-  // below, padrow_geometry) must fit the producer warps, and the band ring
-  // (slots sized by padrow_band_bytes) shared memory next to the weights;
-  // wider images take the im2col kernel
-  const int64_t band0 = (int64_t)g.pad * (g.W + (g.pad > 0 ? g.pad : 1)) + g.pad;
-  const int64_t r8 = (2 * band0 + BM + 7) / 8 * 8;
-  const int64_t planes = c / 32;
-  if (r8 * (planes / 4) > 2 * 32 * PR_NPW || r8 * 16 * planes > 128 * 1024) return false;
-  const int bb = padrow_band_bytes(r8, planes);
-  const int nkb = (int)((k + 255) / 256);
-  if ((filters > 128 ? padrow_smem_bytes<256>(nkb, bb) : padrow_smem_bytes<128>(nkb, bb)) > 227 * 1024) return false;
-  {
-    PadArgs p{};
-    padrow_geometry(p, batch, g.H, g.W, g.kh, g.kw, g.pad);
-    if (!padrow_exact(p)) return false;  // e.g. a 4000 x 4000 1x1 conv: the index split would not be exact
-  }
-  return on && g.stride == 1 && g.Ho == g.H && g.Wo == g.W && g.kh == g.kw && (g.kh & 1) && g.pad == (g.kh - 1) / 2 &&
-         c % 128 == 0 && filters <= 256 && (filters <= 128 ? k <= 1536 : k <= 1280) && g.W < 4096 &&
-         (int64_t)g.kh * g.kw * (c / 64) <= 128 &&
-         // enough tiles to fill the GPU (small batches keep the one-launch path)
-         (int64_t)(g.H + 1) * (g.W + 1) * batch >= (int64_t)BM * num_sms();
+  if (!on || g.stride != 1 || g.Ho != g.H || g.Wo != g.W || g.kh != g.kw || !(g.kh & 1) || g.pad != (g.kh - 1) / 2 ||
+      c % 128 || filters > 256 || (filters <= 128 ? k > 1536 : k > 1280) || g.W >= 4096 || batch > INT32_MAX ||
+      (int64_t)g.kh * g.kw * (c / 64) > 128 ||
+      // enough tiles to fill the GPU (small batches keep the one-launch path)
+      (int64_t)(g.H + 1) * (g.W + 1) * batch < (int64_t)BM * num_sms())
+    return false;
+  p = PadArgs{};
+  padrow_geometry(p, batch, g.H, g.W, g.kh, g.kw, g.pad);
+  if (!padrow_exact(p)) return false;  // e.g. a 4000 x 4000 1x1 conv: the index split would not be exact
+  p.P = c / 32;
+  p.nkb = (int)((k + 255) / 256);
+  p.F = (int)filters;
+  p.kmmas = p.P / 2;
+  // the tile's band must fit the producer warps and one slot's 128 KB, and
+  // the band ring shared memory next to the resident weights
+  if ((int64_t)p.R8 * (p.P / 4) > 2 * 32 * PR_NPW || (int64_t)p.R8 * 16 * p.P > 128 * 1024) return false;
+  p.band_bytes = padrow_band_bytes(p.R8, p.P);
+  return (filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes) : padrow_smem_bytes<128>(p.nkb, p.band_bytes)) <=
+         227 * 1024;
 }
 
 // Row-aligned padded-row plan (tc_padrow.cuh ALIGN): tiles of 128 pixels
@@ -529,6 +532,9 @@ inline bool padrow_ok(const Args& g, int c, int64_t filters, int64_t k, int64_t 
 // eligibility and shapes the launch, so the two cannot drift apart.
 #ifndef B2_PADROW_ALIGN
 #define B2_PADROW_ALIGN 1
+#endif
+#ifndef B2_PADROW_PAIR
+#define B2_PADROW_PAIR 0  // correct but measured slower; B2_PADROW_PAIR=1 opts in
 #endif
 inline bool padrow_align_plan(const Args& g, int c, int64_t filters, int64_t k, int64_t batch, int pool, PadArgs& p,
                               int& smem) {
@@ -569,9 +575,16 @@ inline bool padrow_align_plan(const Args& g, int c, int64_t filters, int64_t k, 
   p.kmmas = p.P / 2;
   p.F = (int)filters;
   p.pool = pool;
+  // CTA pairs (tc_padrow.cuh PAIR): half the weights per CTA, so a deeper band
+  // ring fits; used when there are enough pair tiles for every SM pair
+  static const int pair_env = [] {
+    const char* e = getenv("B2_PADROW_PAIR");
+    return e ? atoi(e) : B2_PADROW_PAIR;
+  }();
+  p.pair = pair_env && batch * h * w / BM >= 2 * (num_sms() / 2) ? 1 : 0;
   for (p.nbands = PR_BANDS_MAX; p.nbands >= min_bands; --p.nbands) {
-    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0)
-                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0);
+    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair)
+                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair);
     if (smem <= 227 * 1024) return true;
   }
   return false;
@@ -657,31 +670,40 @@ inline int padrow_align_run(PadArgs& p, int smem, const void* lines, int sstride
   if (int rc = make_bmap(&map, w, p.F, b_row_bytes, wide ? 256 : 128)) return rc;
   static const bool generic_only = getenv("B2_PR_GENERIC") && atoi(getenv("B2_PR_GENERIC"));  // test hook
   const bool k3 = !generic_only && p.kh == 3 && p.kmmas == 2;
+  const int threads = 32 * (4 + PR_NPW + (wide ? pr_nepi<256, true>() : pr_nepi<128, true>()));
+  const int64_t tiles = (int64_t)p.N * p.HW / BM;
+  if (p.pair) {
+    // weights split over the pair: TMA boxes of BNT / 2 rows
+    if (int rc = make_bmap(&map, w, p.F, b_row_bytes, wide ? 128 : 64)) return rc;
+    void (*kern)(CUtensorMap, PadArgs) =
+        wide ? (k3 ? k_padrow_conv<3, 2, 256, false, true, true> : k_padrow_conv<0, 0, 256, false, true, true>)
+             : (k3 ? k_padrow_conv<3, 2, 128, false, true, true> : k_padrow_conv<0, 0, 128, false, true, true>);
+    static std::atomic<uint64_t> attr2[4];
+    smem_optin(kern, 227 * 1024, attr2[(wide ? 2 : 0) + (k3 ? 1 : 0)]);
+    const int64_t ptiles = (tiles + 1) / 2;
+    const int64_t pairs = ptiles < num_sms() / 2 ? ptiles : num_sms() / 2;
+    launch_kc(2, kern, (unsigned)(2 * pairs), threads, smem, st, map, p);
+    return launched();
+  }
   void (*kern)(CUtensorMap, PadArgs) =
       wide ? (k3 ? k_padrow_conv<3, 2, 256, false, true> : k_padrow_conv<0, 0, 256, false, true>)
            : (k3 ? k_padrow_conv<3, 2, 128, false, true> : k_padrow_conv<0, 0, 128, false, true>);
   static std::atomic<uint64_t> attr[4];
   smem_optin(kern, 227 * 1024, attr[(wide ? 2 : 0) + (k3 ? 1 : 0)]);
-  const int64_t tiles = (int64_t)p.N * p.HW / BM;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  launch_k(kern, grid, 32 * (4 + PR_NPW + (wide ? pr_nepi<256, true>() : pr_nepi<128, true>())), smem, st, map, p);
+  launch_k(kern, grid, threads, smem, st, map, p);
   return launched();
 }
 
-inline int padrow_launch(const Args& g, const void* lines, int64_t batch, int c, const int8_t* w_f4, int64_t filters,
-                         int64_t k, int pool, uint64_t* out, cudaStream_t st) {
-  if (batch > INT32_MAX) return B2_EINVAL;
-  PadArgs p{};
-  padrow_geometry(p, batch, g.H, g.W, g.kh, g.kw, g.pad);
+// launch the virtual-grid kernel planned by padrow_plan (unpooled: pooled
+// layers never take it, see conv_path_f4)
+inline int padrow_launch(PadArgs& p, const Args& g, const void* lines, const int8_t* w_f4, int64_t k, uint64_t* out,
+                         cudaStream_t st) {
   p.x = reinterpret_cast<const uint32_t*>(lines);
   p.sstride = g.sstride;
-  p.P = c / 32;
-  p.nkb = (int)((k + 255) / 256);
-  p.F = (int)filters;
-  p.kmmas = p.P / 2;
   p.thresh = g.thresh;
   p.ge = g.ge;
-  return padrow_run<false>(p, w_f4, kpad_f4(k) / 2, pool, out, st);
+  return padrow_run<false>(p, w_f4, kpad_f4(k) / 2, 0, out, st);
 }
 
 // Kernel choice of the fused fp4 conv (b2_tc4_conv_bn_pack), also exported
@@ -695,7 +717,7 @@ inline int conv_path_f4(const Args& g, int c, int64_t filters, int64_t k, int64_
   // pooled layers the row-aligned kernel cannot take use the im2col kernel's
   // fused pool: the virtual grid's pool windows straddle tiles, and an
   // unpooled scratch would be an allocation inside the forward pass
-  if (!pool && padrow_ok(g, c, filters, k, batch)) return PATH_PADROW;
+  if (!pool && padrow_plan(g, c, filters, k, batch, p)) return PATH_PADROW;
   return PATH_IM2COL;
 }
 
@@ -786,7 +808,7 @@ int conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, cons
     int smem = 0;
     switch (conv_path_f4(g, c, filters, k, batch, pool, p, smem)) {
       case PATH_PADROW_ALIGNED: return padrow_align_run(p, smem, lines, g.sstride, w_i8, kpad_f4(k) / 2, th, out, S(stream));
-      case PATH_PADROW: return padrow_launch(g, lines, batch, c, w_i8, filters, k, pool, out, S(stream));
+      case PATH_PADROW: return padrow_launch(p, g, lines, w_i8, k, out, S(stream));
       default: break;
     }
   }

@@ -1197,8 +1197,9 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     // 256-column accumulator: columns 288..415 for the two warps of a lane
     // quarter) stage half of a warp's chunks during the drain
     constexpr int SPARE0 = 288;
-    // (convolutions: measured 2-3 % faster; dense layers were 7 % slower with it)
-    constexpr bool STAGE_TMEM = F4 && AM == A_CONV && !KS && ECH == 4 && NEPI == 8 && ACC_BUFS == 1 &&
+    // (convolutions: measured 2-3 % faster, and the int32 GEMM; dense layers
+    // with packed output were 7 % slower with it)
+    constexpr bool STAGE_TMEM = F4 && (AM == A_CONV || EM == E_I32) && !KS && ECH == 4 && NEPI == 8 && ACC_BUFS == 1 &&
                                 A_COL0 + F4_SF_COLS <= SPARE0 && SPARE0 + 2 * 64 <= 512 && B2_TMEM_STAGE;
     const int q = warp & 3;                 // EPI0 % 4 == 0: lane quarter
     const int r = q * 32 + lane;

@@ -25,7 +25,7 @@
 #pragma once
 #include <cstdio>
 
-#include "tc_i8.cuh"
+#include "tc_pair.cuh"
 
 namespace b2 {
 namespace tc {
@@ -65,6 +65,7 @@ struct PadArgs {
   int Rb;              // band rows per copy: (128 / W + 2 pad) W
   int nbands;          // band slots in the ring (<= PR_BANDS_MAX)
   int pool;            // fused 2x2/2 max-pool (OR ge / AND le of thresholded bits)
+  int pair;            // CTA-pair launch (PAIR kernel), set by the host plan
 };
 
 #ifndef B2_PADROW_LBO_K
@@ -120,22 +121,33 @@ constexpr int pr_bands() {
   return BNT == 256 ? 3 : PR_BANDS;
 }
 
-template <int KH, int KMMAS, int BNT, bool BYTEIN = false, bool ALIGN = false>
+// PAIR (row-aligned only): a CTA pair on the two SMs of a TPC runs each MMA
+// as M = 256 (cta_group::2): CTA r computes the 128-pixel tile 2 T + r of pair
+// tile T from its own band, and holds half the filters' weights (N / 2 rows),
+// so per SM the MMA reads half the weight bytes and the freed shared memory
+// buys a deeper band ring (MMA-thread timing of the single-CTA conv2: 23 % of
+// its time waiting for a band with three slots).  CTA 1's "band ready" reaches
+// CTA 0's issuer through a relay thread (relaxed remote arrive, see
+// tc_pair.cuh), MMA completion is committed to both CTAs, and both epilogues
+// release the accumulators on CTA 0's barriers.
+template <int KH, int KMMAS, int BNT, bool BYTEIN = false, bool ALIGN = false, bool PAIR = false>
 __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
   constexpr int BN = BNT;
+  constexpr int BNH = PAIR ? BN / 2 : BN;  // weight rows held by this CTA
   constexpr int PR_NEPI = pr_nepi<BNT, ALIGN>();
   constexpr int PR_ACC = pr_acc<BNT>();
   static_assert(!(ALIGN && BYTEIN), "row-aligned tiles take packed-bit input");
+  static_assert(!PAIR || ALIGN, "CTA pairs only on row-aligned tiles");
   const int PR_BANDS = ALIGN ? g.nbands : pr_bands<BNT>();
-  constexpr uint32_t IDESC = idesc_f4(BN);
+  constexpr uint32_t IDESC = PAIR ? idesc_f4_pair(BN) : idesc_f4(BN);
   constexpr int EPI0 = 4 + PR_NPW;
   constexpr int ACC_COLS = BN;
   constexpr int SF_COL = PR_ACC * ACC_COLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sb = smem;                                    // resident weights: nkb atoms of BN x 128 B
-  uint8_t* sband = sb + g.nkb * BN * 128;                // PR_BANDS x band_bytes
+  uint8_t* sb = smem;                                    // resident weights: nkb atoms of BNH x 128 B
+  uint8_t* sband = sb + g.nkb * BNH * 128;               // PR_BANDS x band_bytes
   int4* sthr = reinterpret_cast<int4*>(sband + PR_BANDS * g.band_bytes);  // 64 x (mul, add) pairs
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + BN / 2);
   uint64_t* bres = reinterpret_cast<uint64_t*>(sgm + BN / 32);
@@ -146,27 +158,40 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + PR_ACC);
   uint2* soff = reinterpret_cast<uint2*>(tmem_slot + 2);  // per MMA: (A, B) descriptor address offsets (16 B units)
   uint2* spool = soff + 128;  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND) of horizontal pairs
+  uint64_t* pbfull = reinterpret_cast<uint64_t*>(spool + 2 * BM * (BN / 32));  // PAIR, CTA 0: the peer's band is full
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles = ALIGN ? (int64_t)g.N * g.HW / BM : (g.Vtotal + BM - 1) / BM;
   const uint32_t plane_bytes = (uint32_t)g.R8 * 16u;
+  // this CTA's tiles: t = t_first, t_first + t_step, ... while the pair tile
+  // exists (t - rank < tiles); a PAIR half past the end (odd tile count) is
+  // computed on a zero band and not stored
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int64_t t_first = PAIR ? 2 * (int64_t)(blockIdx.x >> 1) + rank : (int64_t)blockIdx.x;
+  const int64_t t_step = PAIR ? 2 * (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     mbar_init(bres, 1);
     for (int b = 0; b < PR_BANDS; ++b) {
       mbar_init(&bfull[b], PR_NPW);
       mbar_init(&bempty[b], 1);
+      if constexpr (PAIR) mbar_init(&pbfull[b], 1);
     }
     for (int a = 0; a < PR_ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], PR_NEPI);
+      mbar_init(&tempty[a], PAIR ? 2 * PR_NEPI : PR_NEPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -180,18 +205,33 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     tmem_wait_st();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync_all();  // both CTAs' barriers and scale factors exist before any remote access
+  else
+    __syncthreads();
   tc_fence_after();
   pdl_entry();
 
   if (warp == 0) {
-    // ------------------------------------------------ weights, once
+    // ------------------------------------------------ weights, once (PAIR: this CTA's half of the filters)
     if (lane == 0) {
-      mbar_expect_tx(bres, (uint32_t)g.nkb * BN * 128);
-      for (int a = 0; a < g.nkb; ++a) tma_load_2d(sb + a * BN * 128, &bmap, bres, a * 128, 0);
+      mbar_expect_tx(bres, (uint32_t)g.nkb * BNH * 128);
+      for (int a = 0; a < g.nkb; ++a) tma_load_2d(sb + a * BNH * 128, &bmap, bres, a * 128, (int)rank * BNH);
+    }
+  } else if (warp == 1 && PAIR && rank == 1) {
+    // ------------------------------------------------ relay (PAIR, CTA 1): my band is full
+    if (lane == 0) {
+      const uint32_t peer = cluster_map(smem_u32(pbfull), 0);
+      int slot = 0;
+      uint32_t bph = 0;
+      for (int64_t t = t_first; t - rank < tiles; t += t_step) {
+        mbar_wait(&bfull[slot], bph);
+        mbar_arrive_remote(peer + 8u * (uint32_t)slot);
+        if (++slot == PR_BANDS) slot = 0, bph ^= 1;
+      }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
+    // ------------------------------------------------ MMA issuer (PAIR: CTA 0 issues for both)
     if (lane == 0) {
       // descriptor offsets of every MMA of a tile, once: (window cell, K chunk)
       // -> band plane + row shift for A, weight atom + 32-byte step for B
@@ -205,7 +245,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
           for (int kc = 0; kc < g.kmmas; ++kc, ++nmma) {
             const int k = cell * g.P * 32 + kc * 64;  // K element
             soff[nmma] = make_uint2(((uint32_t)(plane0 + 2 * kc) * plane_bytes + (uint32_t)off * 16u) >> 4,
-                                    (uint32_t)((k >> 8) * BN * 128 + ((k & 255) >> 6) * 32) >> 4);
+                                    (uint32_t)((k >> 8) * BNH * 128 + ((k & 255) >> 6) * 32) >> 4);
           }
         }
       mbar_wait(bres, 0);
@@ -215,11 +255,12 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
 #ifdef B2_PR_TIMING
       long long c_band = 0, c_acc = 0, c_issue = 0, c_t0 = clock64();
 #endif
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int64_t t = t_first; t - rank < tiles; t += t_step) {
 #ifdef B2_PR_TIMING
         long long c0 = clock64();
 #endif
         mbar_wait(&bfull[slot], bph);
+        if constexpr (PAIR) mbar_wait(&pbfull[slot], bph);
 #ifdef B2_PR_TIMING
         long long c1 = clock64();
 #endif
@@ -244,21 +285,33 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
                 const uint32_t off = ALIGN ? (uint32_t)(cy << g.wshift) : (uint32_t)(g.band0 + (cy - PAD) * g.Wp + (cx - PAD));
                 const uint32_t plane = ALIGN ? (uint32_t)(cx * 2 * KMMAS + 2 * kc) : (uint32_t)(2 * kc);
                 const uint32_t ao = (plane * plane_bytes + off * 16u) >> 4;
-                const uint32_t bo = (uint32_t)((k >> 8) * BN * 128 + ((k & 255) >> 6) * 32) >> 4;
-                tc_mma_f4(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
-                          (cell | kc) ? 1u : 0u);
+                const uint32_t bo = (uint32_t)((k >> 8) * BNH * 128 + ((k & 255) >> 6) * 32) >> 4;
+                if constexpr (PAIR)
+                  tc_mma_f4_pair(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
+                                 (cell | kc) ? 1u : 0u);
+                else
+                  tc_mma_f4(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
+                            (cell | kc) ? 1u : 0u);
               }
         } else {
           for (int i = 0; i < nmma; ++i) {
             const uint2 o = soff[i];
-            tc_mma_f4(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
+            if constexpr (PAIR)
+              tc_mma_f4_pair(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
+            else
+              tc_mma_f4(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
           }
         }
 #ifdef B2_PR_TIMING
         c_issue += clock64() - c2;
 #endif
-        tc_commit(&bempty[slot]);
-        tc_commit(&tfull[acc]);
+        if constexpr (PAIR) {
+          tc_commit_pair(&bempty[slot]);
+          tc_commit_pair(&tfull[acc]);
+        } else {
+          tc_commit(&bempty[slot]);
+          tc_commit(&tfull[acc]);
+        }
         if (++slot == PR_BANDS) slot = 0, bph ^= 1;
         if (++acc == PR_ACC) acc = 0, aph ^= 1;
       }
@@ -373,17 +426,17 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         const int64_t l0 = lo < 0 ? 0 : lo, h0 = hi > g.HW ? g.HW : hi;
         l2_prefetch(g.x + (n * g.HW + l0) * g.sstride, (uint32_t)((h0 - l0) * g.sstride * 4));
       };
-      for (int i = 1; i < PF_AHEAD; ++i) prefetch(blockIdx.x + (int64_t)i * gridDim.x);
+      for (int i = 1; i < PF_AHEAD; ++i) prefetch(t_first + (int64_t)i * t_step);
       int slot = 0;
       uint32_t ph = 0;
       uint4 wa[UMAX], wb[UMAX];
       bool oka[UMAX], okb[UMAX];
-      load_tile(blockIdx.x, wa, oka);
+      load_tile(t_first, wa, oka);
       // one tile from (wc, okc), loaded one tile earlier; the next tile's
       // loads go into (wn, okn) while this one is stored
       auto tile = [&](int64_t t, uint4 (&wc)[UMAX], bool (&okc)[UMAX], uint4 (&wn)[UMAX], bool (&okn)[UMAX]) {
-        prefetch(t + (int64_t)PF_AHEAD * gridDim.x);
-        load_tile(t + gridDim.x, wn, okn);
+        prefetch(t + (int64_t)PF_AHEAD * t_step);
+        load_tile(t + t_step, wn, okn);
         mbar_wait_suspend(&bempty[slot], ph ^ 1);
         uint8_t* band = sband + slot * g.band_bytes;
 #pragma unroll
@@ -415,9 +468,9 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         if (lane == 0) mbar_arrive(&bfull[slot]);
         if (++slot == PR_BANDS) slot = 0, ph ^= 1;
       };
-      for (int64_t t = blockIdx.x; t < tiles; t += 2 * (int64_t)gridDim.x) {
+      for (int64_t t = t_first; t - rank < tiles; t += 2 * t_step) {
         tile(t, wa, oka, wb, okb);
-        if (t + gridDim.x < tiles) tile(t + gridDim.x, wb, okb, wa, oka);
+        if (t + t_step - rank < tiles) tile(t + t_step, wb, okb, wa, oka);
       }
     } else {
     // each thread owns up to UMAX (band row, 4-word group) units per tile;
@@ -494,7 +547,20 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     uint32_t aph = 0;
     uint32_t it = 0;  // tiles done by this CTA (ALIGN pool buffer parity)
     (void)it;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    // release accumulator `a`: CTA 0's barrier (PAIR: both CTAs' epilogues count)
+    const uint32_t peer_tempty = PAIR && rank ? cluster_map(smem_u32(tempty), 0) : 0u;
+    auto release_acc = [&](int a) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR && rank)
+          mbar_arrive_remote(peer_tempty + 8u * (uint32_t)a);
+        else
+          mbar_arrive(&tempty[a]);
+      }
+    };
+    for (int64_t t = t_first; t - rank < tiles; t += t_step) {
+      const bool tv = t < tiles;  // PAIR: the last pair's second half may lie past the end
 #if B2_PR_EPI_SUSPEND
       mbar_wait_suspend(&tfull[acc], aph);
 #else
@@ -510,11 +576,35 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
 #pragma unroll
         for (int c = 0; c < ECH; ++c) tmem_ld32(ta + c * 32, v[c]);
         tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        release_acc(acc);
 #pragma unroll
         for (int c = 0; c < ECH; ++c) words[c] = thr_word<true>(v[c], sthr + (c0 + c) * 16);
+      } else if constexpr (ECH == 4 && PR_ACC == 1 && B2_TMEM_STAGE) {
+        // the single 256-column accumulator (BNT = 256): stage the first two
+        // chunks in spare TMEM columns (past the accumulator and the scale
+        // factors), load the last two, release — three TMEM round trips —
+        // then threshold from registers / spare (MMA-thread timing: conv3
+        // waited 42 % of its time for the accumulator)
+        const uint32_t spare = tmem + ((uint32_t)(q * 32) << 16) + 288 + ((warp - EPI0) >> 2) * 64;
+        static_assert(SF_COL + 16 <= 288 && 288 + 2 * 64 <= 512, "spare TMEM columns");
+        uint32_t va[32], vb[32];
+        tmem_ld32(ta, va);
+        tmem_ld32(ta + 32, vb);
+        tmem_wait_ld();
+        tmem_st32(spare, va);
+        tmem_st32(spare + 32, vb);
+        tmem_wait_st();
+        tmem_ld32(ta + 64, va);
+        tmem_ld32(ta + 96, vb);
+        tmem_wait_ld();
+        release_acc(acc);
+        words[2] = thr_word<true>(va, sthr + (c0 + 2) * 16);
+        words[3] = thr_word<true>(vb, sthr + (c0 + 3) * 16);
+        tmem_ld32(spare, va);
+        tmem_ld32(spare + 32, vb);
+        tmem_wait_ld();
+        words[0] = thr_word<true>(va, sthr + c0 * 16);
+        words[1] = thr_word<true>(vb, sthr + (c0 + 1) * 16);
       } else {
       // software-pipelined: chunk c + 1 is in flight while chunk c is thresholded
       uint32_t va[32], vb[32];
@@ -528,9 +618,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         words[c] = thr_word<true>(v, sthr + (c0 + c) * 16);
         if (c + 1 < ECH) tmem_wait_ld();
         if (c + 2 == ECH) {  // every chunk is in registers: return the accumulator before the last one's math
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          release_acc(acc);
         }
       }
       }
@@ -538,6 +626,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         const int64_t pix = t * BM + r;  // tiles cover whole images: every row is a pixel
         if (!g.pool) {
           uint32_t* o = g.out_bits + pix * g.ldo32;
+          if (tv)
 #pragma unroll
           for (int c = 0; c < ECH; ++c)
             if (c0 + c < g.ldo32) o[c0 + c] = words[c];
@@ -553,7 +642,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
           }
           epi_bar<PR_NEPI>();
           const int ty = r >> g.wshift, x = r & ((1 << g.wshift) - 1);
-          if (!(ty & 1) && !(x & 1)) {
+          if (tv && !(ty & 1) && !(x & 1)) {
             const int64_t n = pix / g.HW;
             const int y = (int)((pix - n * g.HW) >> g.wshift);
             const int wp = (1 << g.wshift) >> 1;
@@ -585,10 +674,16 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync_all();  // no CTA leaves while its peer can still touch its shared or tensor memory
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -618,10 +713,11 @@ __global__ void k_expand_f4_cells(const uint64_t* __restrict__ w, int64_t rows, 
 }
 
 template <int BNT>
-inline int padrow_smem_bytes(int nkb, int band_bytes, int nbands = pr_bands<BNT>(), bool pool_buf = false) {
-  return nkb * BNT * 128 + nbands * band_bytes + BNT / 2 * 16 + BNT / 8 + 8 * (1 + 2 * PR_BANDS_MAX + 2 * pr_acc<BNT>()) +
-         16 + 8 * 128 +  // MMA offset table (<= 128)
-         (pool_buf ? 2 * BM * (BNT / 32) * 8 : 0) + 1024;
+inline int padrow_smem_bytes(int nkb, int band_bytes, int nbands = pr_bands<BNT>(), bool pool_buf = false,
+                             bool pair = false) {
+  return nkb * (pair ? BNT / 2 : BNT) * 128 + nbands * band_bytes + BNT / 2 * 16 + BNT / 8 +
+         8 * (1 + 2 * PR_BANDS_MAX + 2 * pr_acc<BNT>()) + 16 + 8 * 128 +  // MMA offset table (<= 128)
+         (pool_buf || pair ? 2 * BM * (BNT / 32) * 8 : 0) + (pair ? 8 * PR_BANDS_MAX : 0) + 1024;
 }
 
 // 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for

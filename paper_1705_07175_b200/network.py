@@ -677,6 +677,8 @@ class Network:
         h, w, c = self.input_dims
         return h * w * c
 
+    GROW_LIMIT = 8192  # forward_batch grows a smaller workspace to at most this many images
+
     def _reserve(self, cap: int):
         if cap <= self.cap:
             return
@@ -749,6 +751,11 @@ class Network:
         n = images.shape[0]
         if out is None:
             out = np.empty((n, self.classes), dtype=np.float64)
+        if n > self.cap and self.cap < self.GROW_LIMIT:
+            # a workspace built for fewer images (load() defaults to one) would
+            # run the batch block by block like the reference's per-image loop:
+            # grow it once, up to GROW_LIMIT images
+            self._reserve(min(n, self.GROW_LIMIT))
         for s0 in range(0, n, self.cap):
             self._forward_host_block(images[s0:s0 + self.cap], out[s0:s0 + self.cap])
         return out

@@ -189,3 +189,44 @@ def test_no_allocation_in_forward():
         forward_batch(net, imgs)
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated() == before
+
+
+def test_no_allocation_in_forward_bcnn_timed_kernels():
+    """The bench's kernels (fused first layer, row-aligned padded-row conv
+    with the pool fused, im2col convs, dense) allocate nothing per call: the
+    torch allocator, the device's free memory and the device's default CUDA
+    memory pool (what cudaMallocAsync would draw from) all stay put."""
+    import torch
+    from cuda.bindings import runtime as rt
+    from paper_1705_07175_b200 import _lib
+    assert _lib._so.b2_tc4_conv_path(64, 32, 32, 128, 128, 3, 3, 1, 1, 1) == 3
+    assert _lib._so.b2_tc_byte_conv_path(64, 32, 32, 3, 128, 3, 3, 1, 1, 0) == 1
+    net = Network(zoo.bcnn_spec(), max_batch=64)
+    imgs = np.random.default_rng(3).integers(0, 256, (64, 32, 32, 3), dtype=np.uint8)
+    forward_batch(net, imgs)
+    torch.cuda.synchronize()
+    err, dev = rt.cudaGetDevice()
+    err, pool = rt.cudaDeviceGetDefaultMemPool(dev)
+
+    def pool_reserved():
+        err, v = rt.cudaMemPoolGetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrReservedMemHigh)
+        return int(v)
+
+    before = (torch.cuda.memory_allocated(), torch.cuda.mem_get_info()[0], pool_reserved())
+    for _ in range(5):
+        forward_batch(net, imgs)
+        net.run(64)
+    torch.cuda.synchronize()
+    assert (torch.cuda.memory_allocated(), torch.cuda.mem_get_info()[0], pool_reserved()) == before
+    assert before[2] == 0  # nothing on the network path ever used the stream-ordered pool
+
+
+def test_forward_batch_grows_small_workspace(networks_golden):
+    # ADVICE r1: load() defaults to max_batch=1; a large forward_batch grows
+    # the workspace once instead of running image by image
+    net = load(os.path.join(GOLDEN, "cnn.bdnn"))
+    assert net.cap == 1
+    g = networks_golden
+    got = forward_batch(net, g["cnn_images"])
+    assert net.cap == min(g["cnn_images"].shape[0], net.GROW_LIMIT)
+    assert np.array_equal(got, g["cnn_scores"])
