@@ -582,9 +582,20 @@ inline bool padrow_align_plan(const Args& g, int c, int64_t filters, int64_t k, 
     return e ? atoi(e) : B2_PADROW_PAIR;
   }();
   p.pair = pair_env && batch * h * w / BM >= 2 * (num_sms() / 2) ? 1 : 0;
+  // filters on the MMA's M side with the weights in TMEM (tc_padrow.cuh TW):
+  // <= 128 filters, K / 8 weight columns past PR_TW_COL, pooled rows <= 32 wide
+  static const int tw_env = [] {
+    const char* e = getenv("B2_PADROW_TW");
+    return e ? atoi(e) : 1;
+  }();
+  p.tw = tw_env && !p.pair && filters <= 128 && PR_TW_COL + (k / 8 + 15) / 16 * 16 <= 512 && (!pool || w <= 32) ? 1 : 0;
+  // the producers' input staging ring (PR_RAW_SLOTS bands of raw pixels)
+  if (g.sstride % 4) return false;  // bulk copies move whole 16-byte pixels
+  const int raw = (int)((int64_t)p.Rb * g.sstride * 4);
   for (p.nbands = PR_BANDS_MAX; p.nbands >= min_bands; --p.nbands) {
-    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair)
-                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair);
+    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw)
+           : p.tw        ? padrow_smem_bytes<128>(0, p.band_bytes, p.nbands, pool != 0, false, raw)
+                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw);
     if (smem <= 227 * 1024) return true;
   }
   return false;
@@ -672,6 +683,18 @@ inline int padrow_align_run(PadArgs& p, int smem, const void* lines, int sstride
   const bool k3 = !generic_only && p.kh == 3 && p.kmmas == 2;
   const int threads = 32 * (4 + PR_NPW + (wide ? pr_nepi<256, true>() : pr_nepi<128, true>()));
   const int64_t tiles = (int64_t)p.N * p.HW / BM;
+  if (p.tw) {
+    p.wt = reinterpret_cast<const uint32_t*>(w);
+    p.wt_words = (int)((int64_t)p.kh * p.kw * p.P * 4);  // K / 8
+    p.wt_stride = (int)(b_row_bytes / 4);
+    void (*kern)(CUtensorMap, PadArgs) =
+        k3 ? k_padrow_conv<3, 2, 128, false, true, false, true> : k_padrow_conv<0, 0, 128, false, true, false, true>;
+    static std::atomic<uint64_t> attr3[2];
+    smem_optin(kern, 227 * 1024, attr3[k3 ? 1 : 0]);
+    const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    launch_k(kern, grid, threads, smem, st, map, p);
+    return launched();
+  }
   if (p.pair) {
     // weights split over the pair: TMA boxes of BNT / 2 rows
     if (int rc = make_bmap(&map, w, p.F, b_row_bytes, wide ? 128 : 64)) return rc;

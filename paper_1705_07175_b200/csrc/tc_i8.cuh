@@ -195,6 +195,22 @@ __device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, u
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+#ifndef B2_TC_WARP_ISSUE
+#define B2_TC_WARP_ISSUE 0  // measured slower on the im2col kernel (conv4 3.65 -> 4.26 ms)
+#endif
+// WI: one lane of the converged issuing warp (the lowest active) issues;
+// otherwise the issuing code runs on lane 0 alone
+template <bool WI>
+__device__ __forceinline__ bool pr_elect() {
+  if constexpr (WI) {
+    uint32_t e;
+    asm volatile("{.reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p;}" : "=r"(e));
+    return e != 0;
+  } else {
+    return true;
+  }
+}
+
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -905,7 +921,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (B2_TC_WARP_ISSUE: the whole warp runs the loop with uniform
+    // descriptors, one elected lane issues — see tc_padrow.cuh)
+    constexpr bool WI = B2_TC_WARP_ISSUE != 0;
+    if (WI || lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -942,7 +961,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             const uint32_t as = smem_u32(sa + s * A_STAGE_BYTES);
 #pragma unroll
             for (int k = 0; k < BKS / 64; ++k)
-              if (k < kmma)
+              if (k < kmma && pr_elect<WI>())
                 tc_mma_f4(d, sw128_desc(as + (k >> 2) * BM * BK + (k & 3) * 32),
                           sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, tmem + A_COL0,
                           tmem + A_COL0 + 4, (kb > kb0 || k) ? 1u : 0u);
@@ -951,25 +970,25 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             const uint32_t as = smem_u32(sa + s * A_STAGE_BYTES);
 #pragma unroll
             for (int k = 0; k < BKS / 32; ++k)
-              if (k < kmma)
+              if (k < kmma && pr_elect<WI>())
                 tc_mma_i8_ss(d, sw128_desc(as + (k >> 2) * BM * BK + (k & 3) * 32),
                              sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, (kb > kb0 || k) ? 1u : 0u);
           } else {
             const uint32_t a = tmem + A_COL0 + s * A_STAGE_COLS;
 #pragma unroll
             for (int k = 0; k < BKS / 32; ++k)
-              if (k < kmma)
+              if (k < kmma && pr_elect<WI>())
                 tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC,
                           (kb > kb0 || k) ? 1u : 0u);
           }
-          tc_commit(&empty[s]);
+          if (pr_elect<WI>()) tc_commit(&empty[s]);
           if (++s == SA) s = 0, ph ^= 1;
         }
-        tc_commit(&tfull[acc]);
+        if (pr_elect<WI>()) tc_commit(&tfull[acc]);
         if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
       }
 #ifdef B2_TC_TIMING
-      if (blockIdx.x < 2)
+      if (blockIdx.x < 2 && lane == 0)
         printf("AM %d BN %d: total %lld  wait acc %lld  wait full %lld  items %lld\n", AM, BN, clock64() - c_t0, c_acc,
                c_full, (items - blockIdx.x + gridDim.x - 1) / gridDim.x);
 #endif

@@ -66,6 +66,13 @@ struct PadArgs {
   int nbands;          // band slots in the ring (<= PR_BANDS_MAX)
   int pool;            // fused 2x2/2 max-pool (OR ge / AND le of thresholded bits)
   int pair;            // CTA-pair launch (PAIR kernel), set by the host plan
+  // TW (row-aligned, filters on the MMA's M side): the weights live in TMEM,
+  // read once from these fp4 rows (wt_words 32-bit words = K / 8 of each
+  // row, rows wt_stride words apart)
+  int tw;
+  const uint32_t* wt;
+  int wt_words;
+  int wt_stride;
 };
 
 #ifndef B2_PADROW_LBO_K
@@ -88,17 +95,38 @@ __device__ __forceinline__ void vsplit(const PadArgs& g, int64_t v, int64_t& n, 
 }
 
 constexpr int PR_NPW = 8;       // producer warps
+#ifndef B2_PR_PROD_POLL  // 1: ALIGN producers poll the band-empty barrier instead of suspending
+#define B2_PR_PROD_POLL 0
+#endif
+#if B2_PR_PROD_POLL
+#define B2_PR_PROD_WAIT mbar_wait
+#else
+#define B2_PR_PROD_WAIT mbar_wait_suspend
+#endif
 #ifndef B2_PR_EPI_SUSPEND  // epilogue waits: 1 suspend in hardware, 0 poll
 #define B2_PR_EPI_SUSPEND 0
 #endif
 #ifndef B2_PR_NEPI
 #define B2_PR_NEPI 4
 #endif
+#ifndef B2_PR_WARP_ISSUE
+#define B2_PR_WARP_ISSUE 1
+#endif
 constexpr int PR_NEPI = B2_PR_NEPI;  // epilogue warps: 4 (one per lane quarter) or 8 (two, half the columns each)
 constexpr int PR_BANDS = 4;     // band ring (tiles in flight: hides the band loads' DRAM latency)
 constexpr int PR_ACC = 3;       // accumulator buffers (3 x 128 columns + scale columns)
 constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot (the minimum; wider images take larger slots)
 constexpr int PR_BANDS_MAX = 4;         // barrier slots reserved for the band ring
+constexpr int PR_RAW_SLOTS = 4;         // ALIGN: raw input staging slots (bulk copies 3 tiles ahead)
+
+// 1-D bulk copy global -> shared, completion (bytes) on `bar` (16-byte
+// aligned addresses and size)
+__device__ __forceinline__ void bulk_g2s_pr(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 // KH, KMMAS > 0: compile-time window and K chunks per cell (the issuing
 // thread's 18 descriptor offsets for 3x3 / c = 128 stay in registers and the
@@ -130,15 +158,36 @@ constexpr int pr_bands() {
 // CTA 0's issuer through a relay thread (relaxed remote arrive, see
 // tc_pair.cuh), MMA completion is committed to both CTAs, and both epilogues
 // release the accumulators on CTA 0's barriers.
-template <int KH, int KMMAS, int BNT, bool BYTEIN = false, bool ALIGN = false, bool PAIR = false>
+// TW (row-aligned, BNT = 128, single CTA): the GEMM transposed — D[filter][pixel]
+// = W[filter][k] X[pixel][k] with the weights as the A operand in TMEM (loaded
+// once, columns PR_TW_COL..) and the band as the B operand.  The MMA then reads
+// only the band from shared memory (64 B/clk instead of 128 at N = 128:
+// ncu put the tensor pipe's shared-memory wavefronts plus the producers' and
+// the threshold reads at ~94 % of the shared-memory pipe), the thresholds are
+// per lane (one filter per TMEM lane) and the epilogue transposes sign bits
+// with warp ballots, pooling by shuffles with no shared-memory exchange.
+constexpr int PR_TW_COL = 288;  // first TMEM column of the resident weights (K / 8 columns, <= 224)
+__device__ __forceinline__ void tc_mma_f4_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
+
+template <int KH, int KMMAS, int BNT, bool BYTEIN = false, bool ALIGN = false, bool PAIR = false, bool TW = false>
 __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
   constexpr int BN = BNT;
   constexpr int BNH = PAIR ? BN / 2 : BN;  // weight rows held by this CTA
   constexpr int PR_NEPI = pr_nepi<BNT, ALIGN>();
-  constexpr int PR_ACC = pr_acc<BNT>();
+  constexpr int PR_ACC = TW ? 2 : pr_acc<BNT>();  // TW: 2 x 128 accumulator columns, scales, then the weights
   static_assert(!(ALIGN && BYTEIN), "row-aligned tiles take packed-bit input");
   static_assert(!PAIR || ALIGN, "CTA pairs only on row-aligned tiles");
+  static_assert(!TW || (ALIGN && !PAIR && BNT == 128), "TMEM weights: row-aligned single-CTA 128-pixel tiles");
   const int PR_BANDS = ALIGN ? g.nbands : pr_bands<BNT>();
   constexpr uint32_t IDESC = PAIR ? idesc_f4_pair(BN) : idesc_f4(BN);
   constexpr int EPI0 = 4 + PR_NPW;
@@ -147,7 +196,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sb = smem;                                    // resident weights: nkb atoms of BNH x 128 B
-  uint8_t* sband = sb + g.nkb * BNH * 128;               // PR_BANDS x band_bytes
+  uint8_t* sband = sb + (TW ? 0 : g.nkb * BNH * 128);    // PR_BANDS x band_bytes
   int4* sthr = reinterpret_cast<int4*>(sband + PR_BANDS * g.band_bytes);  // 64 x (mul, add) pairs
   uint32_t* sgm = reinterpret_cast<uint32_t*>(sthr + BN / 2);
   uint64_t* bres = reinterpret_cast<uint64_t*>(sgm + BN / 32);
@@ -159,6 +208,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   uint2* soff = reinterpret_cast<uint2*>(tmem_slot + 2);  // per MMA: (A, B) descriptor address offsets (16 B units)
   uint2* spool = soff + 128;  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND) of horizontal pairs
   uint64_t* pbfull = reinterpret_cast<uint64_t*>(spool + 2 * BM * (BN / 32));  // PAIR, CTA 0: the peer's band is full
+  uint64_t* rfull = pbfull + PR_BANDS_MAX;                                       // ALIGN: raw input staging slot landed
+  uint8_t* sraw = reinterpret_cast<uint8_t*>(rfull + PR_RAW_SLOTS);              // ALIGN: PR_RAW_SLOTS x Rb pixels
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles = ALIGN ? (int64_t)g.N * g.HW / BM : (g.Vtotal + BM - 1) / BM;
@@ -171,12 +222,14 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   const int64_t t_step = PAIR ? 2 * (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(bres, 1);
+    mbar_init(bres, TW ? PR_NEPI : 1);  // TW: every epilogue warp has stored its weight rows
     for (int b = 0; b < PR_BANDS; ++b) {
       mbar_init(&bfull[b], PR_NPW);
       mbar_init(&bempty[b], 1);
       if constexpr (PAIR) mbar_init(&pbfull[b], 1);
     }
+    if constexpr (ALIGN)
+      for (int r = 0; r < PR_RAW_SLOTS; ++r) mbar_init(&rfull[r], 1);
     for (int a = 0; a < PR_ACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], PAIR ? 2 * PR_NEPI : PR_NEPI);
@@ -214,7 +267,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
 
   if (warp == 0) {
     // ------------------------------------------------ weights, once (PAIR: this CTA's half of the filters)
-    if (lane == 0) {
+    if (lane == 0 && !TW) {
       mbar_expect_tx(bres, (uint32_t)g.nkb * BNH * 128);
       for (int a = 0; a < g.nkb; ++a) tma_load_2d(sb + a * BNH * 128, &bmap, bres, a * 128, (int)rank * BNH);
     }
@@ -232,7 +285,14 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (PAIR: CTA 0 issues for both)
-    if (lane == 0) {
+    // B2_PR_WARP_ISSUE: the whole warp runs the issue loop (descriptors are
+    // warp-uniform, so they stay in uniform registers) and one elected lane
+    // issues; a lone lane-0 thread re-broadcast every descriptor (R2UR) per
+    // MMA, and under epilogue load that chain outlasted the 64-cycle MMA
+    // (row-aligned kernels; the virtual-grid 256-column conv3 measured slower
+    // with it: 1.83 vs 1.69 ms)
+    constexpr bool WI = ALIGN && B2_PR_WARP_ISSUE;
+    if (WI || lane == 0) {
       // descriptor offsets of every MMA of a tile, once: (window cell, K chunk)
       // -> band plane + row shift for A, weight atom + 32-byte step for B
       int nmma = 0;
@@ -244,10 +304,12 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
           const int cell = cy * g.kw + cx;
           for (int kc = 0; kc < g.kmmas; ++kc, ++nmma) {
             const int k = cell * g.P * 32 + kc * 64;  // K element
-            soff[nmma] = make_uint2(((uint32_t)(plane0 + 2 * kc) * plane_bytes + (uint32_t)off * 16u) >> 4,
-                                    (uint32_t)((k >> 8) * BNH * 128 + ((k & 255) >> 6) * 32) >> 4);
+            if (lane == 0) soff[nmma] = make_uint2(((uint32_t)(plane0 + 2 * kc) * plane_bytes + (uint32_t)off * 16u) >> 4,
+                                    TW ? (uint32_t)(k >> 3)
+                                       : (uint32_t)((k >> 8) * BNH * 128 + ((k & 255) >> 6) * 32) >> 4);
           }
         }
+      if constexpr (WI) __syncwarp();
       mbar_wait(bres, 0);
       int slot = 0, acc = 0;
       uint32_t bph = 0, aph = 0;
@@ -286,7 +348,11 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
                 const uint32_t plane = ALIGN ? (uint32_t)(cx * 2 * KMMAS + 2 * kc) : (uint32_t)(2 * kc);
                 const uint32_t ao = (plane * plane_bytes + off * 16u) >> 4;
                 const uint32_t bo = (uint32_t)((k >> 8) * BNH * 128 + ((k & 255) >> 6) * 32) >> 4;
-                if constexpr (PAIR)
+                if (!pr_elect<WI>()) {
+                } else if constexpr (TW)
+                  tc_mma_f4_ts(d, tmem + PR_TW_COL + (uint32_t)(k >> 3), adesc0 + ao, IDESC, tmem + SF_COL,
+                               tmem + SF_COL + 4, (cell | kc) ? 1u : 0u);
+                else if constexpr (PAIR)
                   tc_mma_f4_pair(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
                                  (cell | kc) ? 1u : 0u);
                 else
@@ -296,7 +362,11 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         } else {
           for (int i = 0; i < nmma; ++i) {
             const uint2 o = soff[i];
-            if constexpr (PAIR)
+            if (!pr_elect<WI>()) {
+            } else if constexpr (TW)
+              tc_mma_f4_ts(d, tmem + PR_TW_COL + o.y, adesc0 + o.x, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
+                           i ? 1u : 0u);
+            else if constexpr (PAIR)
               tc_mma_f4_pair(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
             else
               tc_mma_f4(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
@@ -305,7 +375,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
 #ifdef B2_PR_TIMING
         c_issue += clock64() - c2;
 #endif
-        if constexpr (PAIR) {
+        if (!pr_elect<WI>()) {
+        } else if constexpr (PAIR) {
           tc_commit_pair(&bempty[slot]);
           tc_commit_pair(&tfull[acc]);
         } else {
@@ -316,7 +387,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         if (++acc == PR_ACC) acc = 0, aph ^= 1;
       }
 #ifdef B2_PR_TIMING
-      if (blockIdx.x < 3)
+      if (blockIdx.x < 3 && lane == 0)
         printf("cta %d: total %lld  wait band %lld  wait acc %lld  issue %lld  tiles %lld\n", blockIdx.x,
                clock64() - c_t0, c_band, c_acc, c_issue, (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 #endif
@@ -395,54 +466,86 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       for (int i = pt; i < PR_BANDS * g.band_bytes / 16; i += 32 * PR_NPW)
         reinterpret_cast<uint4*>(sband)[i] = make_uint4(0, 0, 0, 0);
       asm volatile("bar.sync 2, %0;" ::"n"(32 * PR_NPW) : "memory");  // the clear lands before any copy row is stored
-      auto load_tile = [&](int64_t t, uint4 (&w)[UMAX], bool (&ok)[UMAX]) {
-        const int64_t p0 = t * BM;
-        const int64_t n = p0 / g.HW;
-        const int y0 = (int)((p0 - n * g.HW) >> g.wshift);
-        const uint32_t* img = g.x + n * g.HW * g.sstride;
-#pragma unroll
-        for (int i = 0; i < UMAX; ++i) {
-          const int u = pt + i * 32 * PR_NPW;
-          ok[i] = false;
-          w[i] = make_uint4(0, 0, 0, 0);
-          if (t < tiles && u < units) {
-            const int b = u / groups, grp = u - b * groups;
-            const int y = y0 - g.pad + (b >> g.wshift);
-            if ((unsigned)y < (unsigned)g.H) {
-              ok[i] = true;
-              w[i] = __ldg(reinterpret_cast<const uint4*>(img + ((int64_t)(y << g.wshift) + (b & wmask)) * g.sstride +
-                                                          4 * grp));
-            }
-          }
-        }
-      };
-      // one thread pulls the inputs of the tile PF_AHEAD steps ahead into L2
-      // (a tile's input rows are one contiguous range of the image)
-      constexpr int PF_AHEAD = 4;
-      auto prefetch = [&](int64_t t) {
-        if (pt != 0 || t >= tiles) return;
+      // The tile's input pixels (rows y0 - pad .. y0 + 128/W - 1 + pad of one
+      // image, clamped to the image: one contiguous range) arrive by 1-D bulk
+      // copy into a staging ring RAW_AHEAD tiles ahead of the producers
+      // (register prefetch one tile ahead left ~35 % of the gathers waiting on
+      // DRAM: MMA-thread timing showed 20 % of its time waiting for bands and
+      // the producers busy 97 % of theirs).  Staging row b holds band pixel b.
+      constexpr int RAW_AHEAD = PR_RAW_SLOTS - 1;
+      const uint32_t raw_bytes = (uint32_t)g.Rb * (uint32_t)g.sstride * 4u;
+      auto raw_issue = [&](int64_t t, int rs) {  // one thread
+        if (t - rank >= tiles || t >= tiles) return;
         const int64_t p0 = t * BM, n = p0 / g.HW;
         const int64_t lo = p0 - n * g.HW - (int64_t)g.pad * g.W, hi = lo + g.Rb;
         const int64_t l0 = lo < 0 ? 0 : lo, h0 = hi > g.HW ? g.HW : hi;
-        l2_prefetch(g.x + (n * g.HW + l0) * g.sstride, (uint32_t)((h0 - l0) * g.sstride * 4));
+        const uint32_t bytes = (uint32_t)((h0 - l0) * g.sstride * 4);
+        fence_async_smem();  // the producers' reads of this slot (ordered by their barrier) come first
+        mbar_expect_tx(&rfull[rs], bytes);
+        bulk_g2s_pr(sraw + (size_t)rs * raw_bytes + (size_t)(l0 - lo) * g.sstride * 4, g.x + (n * g.HW + l0) * g.sstride,
+                    bytes, &rfull[rs]);
       };
-      for (int i = 1; i < PF_AHEAD; ++i) prefetch(t_first + (int64_t)i * t_step);
-      int slot = 0;
-      uint32_t ph = 0;
-      uint4 wa[UMAX], wb[UMAX];
-      bool oka[UMAX], okb[UMAX];
-      load_tile(t_first, wa, oka);
-      // one tile from (wc, okc), loaded one tile earlier; the next tile's
-      // loads go into (wn, okn) while this one is stored
-      auto tile = [&](int64_t t, uint4 (&wc)[UMAX], bool (&okc)[UMAX], uint4 (&wn)[UMAX], bool (&okn)[UMAX]) {
-        prefetch(t + (int64_t)PF_AHEAD * t_step);
-        load_tile(t + t_step, wn, okn);
-        mbar_wait_suspend(&bempty[slot], ph ^ 1);
+      if (pt == 0)
+        for (int i = 0; i < RAW_AHEAD; ++i) raw_issue(t_first + (int64_t)i * t_step, i);
+      int slot = 0, rslot = 0;
+      uint32_t ph = 0, rph = 0;
+#ifdef B2_PR_TIMING
+      long long p_wait = 0, p_work = 0, p_sync = 0, p_raw = 0, p_t0 = clock64();
+#endif
+      for (int64_t t = t_first; t - rank < tiles; t += t_step) {
+        // every producer is done with the slot the tile RAW_AHEAD back used
+#ifdef B2_PR_TIMING
+        long long s0 = clock64();
+#endif
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * PR_NPW) : "memory");
+#ifdef B2_PR_TIMING
+        p_sync += clock64() - s0;
+#endif
+        if (pt == 0) raw_issue(t + (int64_t)RAW_AHEAD * t_step, rslot == 0 ? PR_RAW_SLOTS - 1 : rslot - 1);
+        const int64_t p0 = t * BM;
+        const int64_t n = p0 / g.HW;
+        const int y0 = (int)((p0 - n * g.HW) >> g.wshift);
+        const bool tvalid = t < tiles;
+#ifdef B2_PR_TIMING
+        long long r0 = clock64();
+#endif
+        if (tvalid) mbar_wait(&rfull[rslot], rph);
+#ifdef B2_PR_TIMING
+        p_raw += clock64() - r0;
+#endif
+        const uint8_t* raw = sraw + (size_t)rslot * raw_bytes;
+        uint4 wc[UMAX];
+        bool okc[UMAX];
+#pragma unroll
+        for (int i = 0; i < UMAX; ++i) {
+          const int u = pt + i * 32 * PR_NPW;
+          okc[i] = false;
+          wc[i] = make_uint4(0, 0, 0, 0);
+          if (tvalid && u < units) {
+            const int b = u / groups, grp = u - b * groups;
+            const int y = y0 - g.pad + (b >> g.wshift);
+            if ((unsigned)y < (unsigned)g.H) {
+              okc[i] = true;
+              wc[i] = *reinterpret_cast<const uint4*>(raw + (size_t)b * g.sstride * 4 + 16 * grp);
+            }
+          }
+        }
+#ifdef B2_PR_TIMING
+        long long q0 = clock64();
+#endif
+        B2_PR_PROD_WAIT(&bempty[slot], ph ^ 1);
+#ifdef B2_PR_TIMING
+        p_wait += clock64() - q0;
+#endif
         uint8_t* band = sband + slot * g.band_bytes;
 #pragma unroll
         for (int i = 0; i < UMAX; ++i) {
           const int u = pt + i * 32 * PR_NPW;
+#ifdef B2_X_NOSTORE  // experiment: producers skip the band stores
+          if (u < units && wc[i].x == 0x12345678u) {
+#else
           if (u < units) {
+#endif
             const int b = u / groups, grp = u - b * groups;
             const int x = b & wmask;
             uint32_t o[16];
@@ -467,11 +570,14 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bfull[slot]);
         if (++slot == PR_BANDS) slot = 0, ph ^= 1;
-      };
-      for (int64_t t = t_first; t - rank < tiles; t += 2 * t_step) {
-        tile(t, wa, oka, wb, okb);
-        if (t + t_step - rank < tiles) tile(t + t_step, wb, okb, wa, oka);
+        if (++rslot == PR_RAW_SLOTS) rslot = 0, rph ^= 1;
       }
+#ifdef B2_PR_TIMING
+      p_work = clock64() - p_t0 - p_wait;
+      if (blockIdx.x < 2 && (pt == 0 || pt == 255))
+        printf("producer cta %d t%d: total %lld  wait slot %lld  sync %lld  raw %lld  other %lld\n", blockIdx.x, pt,
+               clock64() - p_t0, p_wait, p_sync, p_raw, p_work - p_sync - p_raw);
+#endif
     } else {
     // each thread owns up to UMAX (band row, 4-word group) units per tile;
     // a tile's loads are issued before waiting for its band slot
@@ -527,6 +633,98 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       if (lane == 0) mbar_arrive(&bfull[slot]);
       if (++slot == PR_BANDS) slot = 0, ph ^= 1;
     }
+    }
+  } else if (TW && warp >= EPI0) {
+    // ------------------------------------------------ epilogue, filters on TMEM lanes (TW)
+    static_assert(!TW || SF_COL + 16 <= PR_TW_COL, "TMEM: accumulators, scales, weights");
+    const int q = warp & 3;                 // lane quarter: filters 32 q .. 32 q + 31
+    const int hh = (warp - EPI0) >> 2;      // pixels 64 hh .. 64 hh + 63 of the tile
+    const int f = q * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    {
+      // this warp's half of its 32 filter rows' weights -> TMEM (A operand)
+      const int half = (g.wt_words + 31) / 32 * 16, j0 = hh * half, j1 = min(g.wt_words, j0 + half);
+      const uint32_t* wrow = g.wt + (size_t)f * g.wt_stride;
+      for (int j = j0; j < j1; j += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = (f < g.F && j + i < j1) ? __ldg(wrow + j + i) : 0u;
+        tmem_st16(lane_base + PR_TW_COL + j, v);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bres);
+    }
+    float mul = 0.f, add = -1.f;  // filters past F: bit 0 (the (mul, add) of stage_thresholds)
+    bool ge = true;
+    if (f < g.F) {
+      const int32_t th = __ldg(g.thresh + f);
+      ge = __ldg(g.ge + f) != 0;
+      mul = ge ? 1.f : -1.f;
+      add = (float)(ge ? -th : th);
+    }
+    const uint32_t gm = __ballot_sync(0xffffffffu, ge);  // OR-pool (ge) / AND-pool (le) filters
+    const bool store_q = q < g.ldo32;
+    const int wmask = (1 << g.wshift) - 1;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = t_first; t < tiles; t += t_step) {
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      uint32_t va[32], vb[32];
+      const uint32_t ta = lane_base + acc * ACC_COLS + hh * 64;
+      tmem_ld32(ta, va);
+      tmem_ld32(ta + 32, vb);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+#ifdef B2_X_NOEPI  // experiment: the epilogue only drains
+      if (va[0] != 0x12345678u) { if (++acc == PR_ACC) acc = 0, aph ^= 1; continue; }
+#endif
+      // sign words: lane j ends with the 32-filter word of pixel j (wa) and
+      // pixel 32 + j (wb) of this warp's 64
+      uint32_t wa = 0, wb = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        // bit = sign bit clear, as thr_word (-0 counts as negative)
+        const uint32_t ba = __ballot_sync(0xffffffffu, (int)__float_as_uint(__fmaf_rn(__uint_as_float(va[j]), mul, add)) >= 0);
+        const uint32_t bb = __ballot_sync(0xffffffffu, (int)__float_as_uint(__fmaf_rn(__uint_as_float(vb[j]), mul, add)) >= 0);
+        wa = lane == j ? ba : wa;
+        wb = lane == j ? bb : wb;
+      }
+      const int64_t pix = t * BM + hh * 64 + lane;  // pixel of wa (wb: + 32)
+      if (!g.pool) {
+        if (store_q) {
+          g.out_bits[pix * g.ldo32 + q] = wa;
+          g.out_bits[(pix + 32) * g.ldo32 + q] = wb;
+        }
+      } else {
+        // 2x2/2 pool: vertical partner in wb (W = 32) or lane ^ W (W <= 16),
+        // horizontal partner lane ^ 1; the top-left lane of each window stores
+        const int x = lane & wmask;
+        const int wp = (1 << g.wshift) >> 1;
+        auto store_pooled = [&](uint32_t o, uint32_t an, int64_t px, bool top) {
+          o |= __shfl_xor_sync(0xffffffffu, o, 1);
+          an &= __shfl_xor_sync(0xffffffffu, an, 1);
+          if (store_q && top && !(x & 1)) {
+            const int64_t n = px / g.HW;
+            const int y = (int)((px - n * g.HW) >> g.wshift);
+            g.out_bits[((n * (g.H >> 1) + (y >> 1)) * wp + (x >> 1)) * g.ldo32 + q] = (o & gm) | (an & ~gm);
+          }
+        };
+        if (g.wshift == 5) {
+          store_pooled(wa | wb, wa & wb, pix, true);
+        } else {
+          const int vs = 1 << g.wshift;
+          const bool top = !(lane & vs);
+          const uint32_t wa2 = __shfl_xor_sync(0xffffffffu, wa, vs), wb2 = __shfl_xor_sync(0xffffffffu, wb, vs);
+          store_pooled(wa | wa2, wa & wa2, pix, top);
+          store_pooled(wb | wb2, wb & wb2, pix + 32, top);
+        }
+      }
+      if (++acc == PR_ACC) acc = 0, aph ^= 1;
     }
   } else if (warp >= EPI0) {
     // ------------------------------------------------ epilogue
@@ -712,12 +910,15 @@ __global__ void k_expand_f4_cells(const uint64_t* __restrict__ w, int64_t rows, 
   out[t] = word;
 }
 
+// raw_bytes > 0 (ALIGN): the spool region is always laid out (the staging
+// ring and its barriers follow it)
 template <int BNT>
 inline int padrow_smem_bytes(int nkb, int band_bytes, int nbands = pr_bands<BNT>(), bool pool_buf = false,
-                             bool pair = false) {
+                             bool pair = false, int raw_bytes = 0) {
   return nkb * (pair ? BNT / 2 : BNT) * 128 + nbands * band_bytes + BNT / 2 * 16 + BNT / 8 +
          8 * (1 + 2 * PR_BANDS_MAX + 2 * pr_acc<BNT>()) + 16 + 8 * 128 +  // MMA offset table (<= 128)
-         (pool_buf || pair ? 2 * BM * (BNT / 32) * 8 : 0) + (pair ? 8 * PR_BANDS_MAX : 0) + 1024;
+         (pool_buf || pair || raw_bytes ? 2 * BM * (BNT / 32) * 8 : 0) + (pair || raw_bytes ? 8 * PR_BANDS_MAX : 0) +
+         (raw_bytes ? 8 * PR_RAW_SLOTS + PR_RAW_SLOTS * raw_bytes : 0) + 1024;
 }
 
 // 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for
