@@ -584,11 +584,23 @@ inline bool padrow_align_plan(const Args& g, int c, int64_t filters, int64_t k, 
   p.pair = pair_env && batch * h * w / BM >= 2 * (num_sms() / 2) ? 1 : 0;
   // filters on the MMA's M side with the weights in TMEM (tc_padrow.cuh TW):
   // <= 128 filters, K / 8 weight columns past PR_TW_COL, pooled rows <= 32 wide
+  // (opt-in: with the loader warp the weights-in-shared-memory form is faster,
+  // conv2 3.57 vs 3.94 ms — the per-lane ballot epilogue costs more issue
+  // slots than the shared-memory bandwidth it saves)
   static const int tw_env = [] {
     const char* e = getenv("B2_PADROW_TW");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   p.tw = tw_env && !p.pair && filters <= 128 && PR_TW_COL + (k / 8 + 15) / 16 * 16 <= 512 && (!pool || w <= 32) ? 1 : 0;
+  // single-CTA weights-in-shared-memory kernels fold the threshold into one
+  // more K = 64 MMA (tc_padrow.cuh BIAS): its block may need one more atom,
+  // and the bias (|T| + 1 <= K + 1) must fit the two-block encoding
+  p.kk = (int)k;
+  p.nkb_ld = p.nkb;
+  if (!p.tw && !p.pair) {
+    if (k > 5760 || k % 64) return false;
+    p.nkb = (int)((k + 64 + 255) / 256);
+  }
   // the producers' input staging ring (PR_RAW_SLOTS bands of raw pixels)
   if (g.sstride % 4) return false;  // bulk copies move whole 16-byte pixels
   const int raw = (int)((int64_t)p.Rb * g.sstride * 4);

@@ -41,6 +41,8 @@ struct PadArgs {
   int R8;              // band rows (multiple of 8): 128 + 2 * band0
   int band0;           // halo above a tile: pad * Wp + pad virtual rows
   int nkb;             // 128-byte B atoms (256 K elements) in shared memory
+  int nkb_ld;          // ALIGN: atoms loaded from the weights (nkb may add one for the threshold block); 0 = nkb
+  int kk;              // ALIGN: K = kh kw c (the threshold block's first K element)
   int band_bytes;      // band slot stride: max(PR_BAND_MAX, R8 * 16 * planes) rounded to 1 KB
   int F;               // filters (<= 128)
   int kmmas;           // K=64 MMAs per window cell (= P / 2)
@@ -95,13 +97,18 @@ __device__ __forceinline__ void vsplit(const PadArgs& g, int64_t v, int64_t& n, 
 }
 
 constexpr int PR_NPW = 8;       // producer warps
-#ifndef B2_PR_PROD_POLL  // 1: ALIGN producers poll the band-empty barrier instead of suspending
+#ifndef B2_PR_PROD_POLL  // ALIGN producers' band-empty wait: 0 back off (nanosleep), 1 poll, 2 suspend hint
 #define B2_PR_PROD_POLL 0
 #endif
-#if B2_PR_PROD_POLL
-#define B2_PR_PROD_WAIT mbar_wait
+#ifndef B2_PR_SLEEP_NS  // back-off of the ALIGN loader / producer waits (ncu: the suspend-hinted try_wait
+#define B2_PR_SLEEP_NS 128  // still retried ~25 times per tile per warp, ~11 % of the kernel's issued instructions)
+#endif
+#if B2_PR_PROD_POLL == 1
+#define B2_PR_PROD_WAIT(b, p) mbar_wait(b, p)
+#elif B2_PR_PROD_POLL == 2
+#define B2_PR_PROD_WAIT(b, p) mbar_wait_suspend(b, p)
 #else
-#define B2_PR_PROD_WAIT mbar_wait_suspend
+#define B2_PR_PROD_WAIT(b, p) mbar_wait_sleep(b, p, B2_PR_SLEEP_NS)
 #endif
 #ifndef B2_PR_EPI_SUSPEND  // epilogue waits: 1 suspend in hardware, 0 poll
 #define B2_PR_EPI_SUSPEND 0
@@ -158,6 +165,48 @@ constexpr int pr_bands() {
 // CTA 0's issuer through a relay thread (relaxed remote arrive, see
 // tc_pair.cuh), MMA completion is committed to both CTAs, and both epilogues
 // release the accumulators on CTA 0's barriers.
+// Threshold folded into the GEMM (row-aligned single-CTA kernels): one more
+// K = 64 MMA per tile adds a per-filter integer bias -T' to every
+// accumulator, so the epilogue only collects sign bits (ncu: the kernel was
+// issue-bound and the (mul, add) threshold pass was a third of the
+// epilogue's instructions).  A = a constant +1 block, B = the filter's 64
+// bias elements: block 0 (scale 2^5) holds 16 q, block 1 (scale 2^0) the rest
+// r, with b = 16 q + r.  T' = T (ge: bit = acc >= T, i.e. sign clear) or
+// T + 1 (le: bit = acc <= T, i.e. sign set), clamped to +-(K + 1).
+constexpr uint32_t PR_BIAS_SF = 0x7F7F7F84u;  // scale bytes: block 0 2^5, block 1 2^0
+// e2m1 magnitudes of a count of half units (<= 11): up to two codes
+__device__ __forceinline__ void pr_half_units(int h, int& c0, int& c1) {
+  // 0.5 1 1.5 2 3 4 6 -> codes 1..7 = 1 2 3 4 6 8 12 half units
+  static constexpr int8_t a[12] = {0, 1, 2, 3, 4, 4, 5, 5, 6, 6, 6, 6};
+  static constexpr int8_t b[12] = {0, 0, 0, 0, 0, 1, 0, 1, 0, 1, 2, 3};
+  c0 = a[h], c1 = b[h];
+}
+// 32 e2m1 codes (one scale block) summing to sign * h half units, h <= 30 * 12 + 11
+__device__ __forceinline__ uint4 pr_bias_block(int h, bool neg) {
+  uint32_t w[4] = {0, 0, 0, 0};
+  const uint32_t sg = neg ? 8u : 0u;
+  int e = 0;
+  for (; h >= 12; h -= 12, ++e) w[e >> 3] |= (7u | sg) << (4 * (e & 7));
+  int c0, c1;
+  pr_half_units(h, c0, c1);
+  if (c0) w[e >> 3] |= ((uint32_t)c0 | sg) << (4 * (e & 7)), ++e;
+  if (c1) w[e >> 3] |= ((uint32_t)c1 | sg) << (4 * (e & 7)), ++e;
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// the 32 bytes of filter n's threshold block
+__device__ __forceinline__ void pr_bias_bytes(int64_t bias, uint4& blk0, uint4& blk1) {
+  const int64_t q = bias / 16, r = bias - 16 * q;  // |r| < 16
+  blk0 = pr_bias_block((int)(q < 0 ? -q : q), q < 0);        // q half units of 2^5 = 16 q
+  blk1 = pr_bias_block((int)(2 * (r < 0 ? -r : r)), r < 0);  // 2 |r| half units of 2^0 = r
+}
+// sign word of 32 accumulators: bit j = sign bit of v[j]
+__device__ __forceinline__ uint32_t sign_word(const uint32_t (&v)[32]) {
+  uint32_t sg = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) sg = __funnelshift_l(v[j], sg, 1);
+  return __brev(sg);
+}
+
 // TW (row-aligned, BNT = 128, single CTA): the GEMM transposed — D[filter][pixel]
 // = W[filter][k] X[pixel][k] with the weights as the A operand in TMEM (loaded
 // once, columns PR_TW_COL..) and the band as the B operand.  The MMA then reads
@@ -188,11 +237,14 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   static_assert(!(ALIGN && BYTEIN), "row-aligned tiles take packed-bit input");
   static_assert(!PAIR || ALIGN, "CTA pairs only on row-aligned tiles");
   static_assert(!TW || (ALIGN && !PAIR && BNT == 128), "TMEM weights: row-aligned single-CTA 128-pixel tiles");
+  constexpr bool BIAS = ALIGN && !PAIR && !TW;  // threshold folded into the GEMM
   const int PR_BANDS = ALIGN ? g.nbands : pr_bands<BNT>();
   constexpr uint32_t IDESC = PAIR ? idesc_f4_pair(BN) : idesc_f4(BN);
   constexpr int EPI0 = 4 + PR_NPW;
   constexpr int ACC_COLS = BN;
   constexpr int SF_COL = PR_ACC * ACC_COLS;
+  constexpr int SF_BIAS = SF_COL + 16;  // BIAS: the threshold block's B scales (16 columns)
+  static_assert(!BIAS || SF_BIAS + 16 <= (BNT == 256 ? 288 : 512), "TMEM: scale columns");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sb = smem;                                    // resident weights: nkb atoms of BNH x 128 B
@@ -209,7 +261,13 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   uint2* spool = soff + 128;  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND) of horizontal pairs
   uint64_t* pbfull = reinterpret_cast<uint64_t*>(spool + 2 * BM * (BN / 32));  // PAIR, CTA 0: the peer's band is full
   uint64_t* rfull = pbfull + PR_BANDS_MAX;                                       // ALIGN: raw input staging slot landed
-  uint8_t* sraw = reinterpret_cast<uint8_t*>(rfull + PR_RAW_SLOTS);              // ALIGN: PR_RAW_SLOTS x Rb pixels
+  uint64_t* rempty = rfull + PR_RAW_SLOTS;                                       // ALIGN: every producer warp read it
+  uint8_t* sraw = reinterpret_cast<uint8_t*>(rempty + PR_RAW_SLOTS);
+  sraw += (16u - (smem_u32(sraw) & 15u)) & 15u;
+  uint64_t* bbias = reinterpret_cast<uint64_t*>(sraw + PR_RAW_SLOTS * g.Rb * g.sstride * 4);  // BIAS: block written
+  uint8_t* sones = reinterpret_cast<uint8_t*>(bbias + 2);  // BIAS: 128 rows x 64 e2m1 +1 (4 KB, no swizzle)
+  sones += (128u - (smem_u32(sones) & 127u)) & 127u;
+  // ^ ALIGN: PR_RAW_SLOTS x Rb pixels (16-byte aligned bulk-copy targets)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles = ALIGN ? (int64_t)g.N * g.HW / BM : (g.Vtotal + BM - 1) / BM;
@@ -228,8 +286,12 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       mbar_init(&bempty[b], 1);
       if constexpr (PAIR) mbar_init(&pbfull[b], 1);
     }
+    if constexpr (BIAS) mbar_init(bbias, 1);
     if constexpr (ALIGN)
-      for (int r = 0; r < PR_RAW_SLOTS; ++r) mbar_init(&rfull[r], 1);
+      for (int r = 0; r < PR_RAW_SLOTS; ++r) {
+        mbar_init(&rfull[r], 1);
+        mbar_init(&rempty[r], PR_NPW);
+      }
     for (int a = 0; a < PR_ACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], PAIR ? 2 * PR_NEPI : PR_NEPI);
@@ -255,6 +317,11 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
 #pragma unroll
     for (int i = 0; i < 16; ++i) ones[i] = 0x7F7F7F7Fu;
     tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + SF_COL, ones);
+    if constexpr (BIAS) {  // every lane quarter holds the B scales of all N rows (n % 32, column n / 32)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) ones[i] = PR_BIAS_SF;
+      tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + SF_BIAS, ones);
+    }
     tmem_wait_st();
   }
   tc_fence_before();
@@ -267,9 +334,58 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
 
   if (warp == 0) {
     // ------------------------------------------------ weights, once (PAIR: this CTA's half of the filters)
+    const int nkb_ld = ALIGN && g.nkb_ld ? g.nkb_ld : g.nkb;
     if (lane == 0 && !TW) {
-      mbar_expect_tx(bres, (uint32_t)g.nkb * BNH * 128);
-      for (int a = 0; a < g.nkb; ++a) tma_load_2d(sb + a * BNH * 128, &bmap, bres, a * 128, (int)rank * BNH);
+      mbar_expect_tx(bres, (uint32_t)nkb_ld * BNH * 128);
+      for (int a = 0; a < nkb_ld; ++a) tma_load_2d(sb + a * BNH * 128, &bmap, bres, a * 128, (int)rank * BNH);
+    }
+    if constexpr (BIAS) {
+      // each filter's threshold block at K = kk .. kk + 63 of its weight row
+      // (128-byte swizzled atoms: 16-byte chunk c of row n at c ^ (n & 7))
+      mbar_wait(bres, 0);
+      const int a = g.kk >> 8, ch = ((g.kk & 255) >> 1) >> 4;
+      const int64_t kmax = g.kk + 1;
+      for (int n = lane; n < BN; n += 32) {
+        int64_t b = -1;  // padding filters: bit 0 (ge with sign set)
+        if (n < g.F) {
+          const int64_t th = __ldg(g.thresh + n);
+          b = __ldg(g.ge + n) ? -th : -(th + 1);
+          b = b > kmax ? kmax : (b < -kmax ? -kmax : b);
+        }
+        uint4 b0, b1;
+        pr_bias_bytes(b, b0, b1);
+        uint8_t* row = sb + a * BNH * 128 + (n >> 3) * 1024 + (n & 7) * 128;
+        *reinterpret_cast<uint4*>(row + ((ch ^ (n & 7)) << 4)) = b0;
+        *reinterpret_cast<uint4*>(row + (((ch + 1) ^ (n & 7)) << 4)) = b1;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bbias);
+    }
+  } else if (ALIGN && warp == 3) {
+    // ------------------------------------------------ input loader (ALIGN)
+    // The tile's input pixels (rows y0 - pad .. y0 + 128/W - 1 + pad of one
+    // image, clamped to the image: one contiguous range) arrive by 1-D bulk
+    // copy into a ring of PR_RAW_SLOTS staging slots that the producer warps
+    // release one by one (a per-tile named barrier among the producers, with
+    // one of them issuing the copies, held every producer to the slowest:
+    // ncu put the producers' top stall on that barrier).  Staging row b holds
+    // band pixel b.
+    if (lane == 0) {
+      const uint32_t raw_bytes = (uint32_t)g.Rb * (uint32_t)g.sstride * 4u;
+      int rs = 0;
+      uint32_t rph = 0;
+      for (int64_t t = t_first; t < tiles; t += t_step) {
+        mbar_wait_sleep(&rempty[rs], rph ^ 1, B2_PR_SLEEP_NS);  // (polling cost ~180 issue slots per tile)
+        const int64_t p0 = t * BM, n = p0 / g.HW;
+        const int64_t lo = p0 - n * g.HW - (int64_t)g.pad * g.W, hi = lo + g.Rb;
+        const int64_t l0 = lo < 0 ? 0 : lo, h0 = hi > g.HW ? g.HW : hi;
+        const uint32_t bytes = (uint32_t)((h0 - l0) * g.sstride * 4);
+        mbar_expect_tx(&rfull[rs], bytes);
+        bulk_g2s_pr(sraw + (size_t)rs * raw_bytes + (size_t)(l0 - lo) * g.sstride * 4, g.x + (n * g.HW + l0) * g.sstride,
+                    bytes, &rfull[rs]);
+        if (++rs == PR_RAW_SLOTS) rs = 0, rph ^= 1;
+      }
     }
   } else if (warp == 1 && PAIR && rank == 1) {
     // ------------------------------------------------ relay (PAIR, CTA 1): my band is full
@@ -311,9 +427,14 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         }
       if constexpr (WI) __syncwarp();
       mbar_wait(bres, 0);
+      if constexpr (BIAS) mbar_wait(bbias, 0);
+      const uint64_t ones_desc = noswz_desc(smem_u32(sones), 2048);
+      const uint32_t bias_bo = BIAS ? (uint32_t)((g.kk >> 8) * BNH * 128 + ((g.kk & 255) >> 6) * 32) >> 4 : 0u;
       int slot = 0, acc = 0;
       uint32_t bph = 0, aph = 0;
       const uint64_t bdesc0 = sw128_desc(smem_u32(sb));
+      const uint32_t b_lo = (uint32_t)bdesc0, b_hi = (uint32_t)(bdesc0 >> 32);
+      const uint32_t tm = WI ? __shfl_sync(0xffffffffu, tmem, 0) : tmem;  // warp-uniform TMEM base
 #ifdef B2_PR_TIMING
       long long c_band = 0, c_acc = 0, c_issue = 0, c_t0 = clock64();
 #endif
@@ -332,8 +453,15 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         c_band += c1 - c0, c_acc += c2 - c1;
 #endif
         tc_fence_after();
-        const uint32_t d = tmem + acc * ACC_COLS;
+        // descriptors as (lo + offset, hi): the offsets only touch the 14-bit
+        // start-address field; with tm broadcast from lane 0 every operand is
+        // warp-uniform and the issue sequence stays in uniform registers
+        const uint32_t d = tm + acc * ACC_COLS;
         const uint64_t adesc0 = noswz_desc(smem_u32(sband + slot * g.band_bytes), plane_bytes);
+        const uint32_t a_lo = (uint32_t)adesc0, a_hi = (uint32_t)(adesc0 >> 32);
+        auto dsc = [](uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; };
+        const bool leader = pr_elect<WI>();
+        if (leader) {
         if constexpr (KH > 0) {
           constexpr int PAD = KH / 2;
 #pragma unroll
@@ -348,34 +476,37 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
                 const uint32_t plane = ALIGN ? (uint32_t)(cx * 2 * KMMAS + 2 * kc) : (uint32_t)(2 * kc);
                 const uint32_t ao = (plane * plane_bytes + off * 16u) >> 4;
                 const uint32_t bo = (uint32_t)((k >> 8) * BNH * 128 + ((k & 255) >> 6) * 32) >> 4;
-                if (!pr_elect<WI>()) {
-                } else if constexpr (TW)
-                  tc_mma_f4_ts(d, tmem + PR_TW_COL + (uint32_t)(k >> 3), adesc0 + ao, IDESC, tmem + SF_COL,
-                               tmem + SF_COL + 4, (cell | kc) ? 1u : 0u);
+                if constexpr (TW)
+                  tc_mma_f4_ts(d, tm + PR_TW_COL + (uint32_t)(k >> 3), dsc(a_lo + ao, a_hi), IDESC, tm + SF_COL,
+                               tm + SF_COL + 4, (cell | kc) ? 1u : 0u);
                 else if constexpr (PAIR)
-                  tc_mma_f4_pair(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
+                  tc_mma_f4_pair(d, dsc(a_lo + ao, a_hi), dsc(b_lo + bo, b_hi), IDESC, tm + SF_COL, tm + SF_COL + 4,
                                  (cell | kc) ? 1u : 0u);
                 else
-                  tc_mma_f4(d, adesc0 + ao, bdesc0 + bo, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
+                  tc_mma_f4(d, dsc(a_lo + ao, a_hi), dsc(b_lo + bo, b_hi), IDESC, tm + SF_COL, tm + SF_COL + 4,
                             (cell | kc) ? 1u : 0u);
               }
         } else {
           for (int i = 0; i < nmma; ++i) {
             const uint2 o = soff[i];
-            if (!pr_elect<WI>()) {
-            } else if constexpr (TW)
-              tc_mma_f4_ts(d, tmem + PR_TW_COL + o.y, adesc0 + o.x, IDESC, tmem + SF_COL, tmem + SF_COL + 4,
+            if constexpr (TW)
+              tc_mma_f4_ts(d, tm + PR_TW_COL + o.y, dsc(a_lo + o.x, a_hi), IDESC, tm + SF_COL, tm + SF_COL + 4,
                            i ? 1u : 0u);
             else if constexpr (PAIR)
-              tc_mma_f4_pair(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
+              tc_mma_f4_pair(d, dsc(a_lo + o.x, a_hi), dsc(b_lo + o.y, b_hi), IDESC, tm + SF_COL, tm + SF_COL + 4,
+                             i ? 1u : 0u);
             else
-              tc_mma_f4(d, adesc0 + o.x, bdesc0 + o.y, IDESC, tmem + SF_COL, tmem + SF_COL + 4, i ? 1u : 0u);
+              tc_mma_f4(d, dsc(a_lo + o.x, a_hi), dsc(b_lo + o.y, b_hi), IDESC, tm + SF_COL, tm + SF_COL + 4,
+                        i ? 1u : 0u);
           }
+        }
+        if constexpr (BIAS)
+          tc_mma_f4(d, ones_desc, dsc(b_lo + bias_bo, b_hi), IDESC, tm + SF_COL, tm + SF_BIAS, 1u);
         }
 #ifdef B2_PR_TIMING
         c_issue += clock64() - c2;
 #endif
-        if (!pr_elect<WI>()) {
+        if (!leader) {
         } else if constexpr (PAIR) {
           tc_commit_pair(&bempty[slot]);
           tc_commit_pair(&tfull[acc]);
@@ -459,52 +590,31 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       // written (register double buffer), so their latency overlaps.
       constexpr int UMAX = 2;
       const int pt = (warp - 4) * 32 + lane;  // 0 .. 255
-      const int groups = g.P / 4;
+      const int groups = KH > 0 ? KMMAS / 2 : g.P / 4;  // compile-time for the 3x3 kernels (no division below)
       const int units = g.Rb * groups;
       const int kwc = KH > 0 ? KH : g.kw;
       const int wmask = (1 << g.wshift) - 1;
       for (int i = pt; i < PR_BANDS * g.band_bytes / 16; i += 32 * PR_NPW)
         reinterpret_cast<uint4*>(sband)[i] = make_uint4(0, 0, 0, 0);
+      if constexpr (BIAS)  // the threshold block's +1 operand (published with the first band)
+        for (int i = pt; i < 4096 / 16; i += 32 * PR_NPW)
+          reinterpret_cast<uint4*>(sones)[i] = make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u);
       asm volatile("bar.sync 2, %0;" ::"n"(32 * PR_NPW) : "memory");  // the clear lands before any copy row is stored
-      // The tile's input pixels (rows y0 - pad .. y0 + 128/W - 1 + pad of one
-      // image, clamped to the image: one contiguous range) arrive by 1-D bulk
-      // copy into a staging ring RAW_AHEAD tiles ahead of the producers
-      // (register prefetch one tile ahead left ~35 % of the gathers waiting on
-      // DRAM: MMA-thread timing showed 20 % of its time waiting for bands and
-      // the producers busy 97 % of theirs).  Staging row b holds band pixel b.
-      constexpr int RAW_AHEAD = PR_RAW_SLOTS - 1;
+      // input pixels from the loader warp's staging ring
       const uint32_t raw_bytes = (uint32_t)g.Rb * (uint32_t)g.sstride * 4u;
-      auto raw_issue = [&](int64_t t, int rs) {  // one thread
-        if (t - rank >= tiles || t >= tiles) return;
-        const int64_t p0 = t * BM, n = p0 / g.HW;
-        const int64_t lo = p0 - n * g.HW - (int64_t)g.pad * g.W, hi = lo + g.Rb;
-        const int64_t l0 = lo < 0 ? 0 : lo, h0 = hi > g.HW ? g.HW : hi;
-        const uint32_t bytes = (uint32_t)((h0 - l0) * g.sstride * 4);
-        fence_async_smem();  // the producers' reads of this slot (ordered by their barrier) come first
-        mbar_expect_tx(&rfull[rs], bytes);
-        bulk_g2s_pr(sraw + (size_t)rs * raw_bytes + (size_t)(l0 - lo) * g.sstride * 4, g.x + (n * g.HW + l0) * g.sstride,
-                    bytes, &rfull[rs]);
-      };
-      if (pt == 0)
-        for (int i = 0; i < RAW_AHEAD; ++i) raw_issue(t_first + (int64_t)i * t_step, i);
       int slot = 0, rslot = 0;
       uint32_t ph = 0, rph = 0;
 #ifdef B2_PR_TIMING
       long long p_wait = 0, p_work = 0, p_sync = 0, p_raw = 0, p_t0 = clock64();
 #endif
+      // tile t = image t / tpi, first row (t % tpi) * BM / W: stepped
+      // incrementally (a 64-bit division per tile was ~25 instructions)
+      const int tpi = (int)(g.HW / BM), trows = BM >> g.wshift;
+      const int step_r = (int)(t_step % tpi);
+      int tr = (int)(t_first % tpi);
       for (int64_t t = t_first; t - rank < tiles; t += t_step) {
-        // every producer is done with the slot the tile RAW_AHEAD back used
-#ifdef B2_PR_TIMING
-        long long s0 = clock64();
-#endif
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * PR_NPW) : "memory");
-#ifdef B2_PR_TIMING
-        p_sync += clock64() - s0;
-#endif
-        if (pt == 0) raw_issue(t + (int64_t)RAW_AHEAD * t_step, rslot == 0 ? PR_RAW_SLOTS - 1 : rslot - 1);
-        const int64_t p0 = t * BM;
-        const int64_t n = p0 / g.HW;
-        const int y0 = (int)((p0 - n * g.HW) >> g.wshift);
+        const int y0 = tr * trows;
+        if ((tr += step_r) >= tpi) tr -= tpi;
         const bool tvalid = t < tiles;
 #ifdef B2_PR_TIMING
         long long r0 = clock64();
@@ -530,6 +640,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
             }
           }
         }
+        __syncwarp();
+        if (tvalid && lane == 0) mbar_arrive(&rempty[rslot]);  // the staging slot may be refilled
 #ifdef B2_PR_TIMING
         long long q0 = clock64();
 #endif
@@ -583,7 +695,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     // a tile's loads are issued before waiting for its band slot
     constexpr int UMAX = 2;
     const int pt = (warp - 4) * 32 + lane;  // 0 .. 255
-    const int groups = g.P / 4;             // 4-word groups per pixel
+    const int groups = KH > 0 ? KMMAS / 2 : g.P / 4;  // 4-word groups per pixel
     const int units = g.R8 * groups;
     int slot = 0;
     uint32_t ph = 0;
@@ -709,9 +821,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
           o |= __shfl_xor_sync(0xffffffffu, o, 1);
           an &= __shfl_xor_sync(0xffffffffu, an, 1);
           if (store_q && top && !(x & 1)) {
-            const int64_t n = px / g.HW;
-            const int y = (int)((px - n * g.HW) >> g.wshift);
-            g.out_bits[((n * (g.H >> 1) + (y >> 1)) * wp + (x >> 1)) * g.ldo32 + q] = (o & gm) | (an & ~gm);
+            const int ty = (int)(px - t * BM) >> g.wshift;  // row within the tile (tiles are whole row pairs)
+            g.out_bits[(t * (BM / 4) + (ty >> 1) * wp + (x >> 1)) * g.ldo32 + q] = (o & gm) | (an & ~gm);
           }
         };
         if (g.wshift == 5) {
@@ -741,6 +852,14 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       stage_thresholds<true>(ga, 0, BN, et, 32 * PR_NEPI, lane, sthr, sgm);
     }
     epi_bar<PR_NEPI>();
+    // sign word of accumulator chunk ch: BIAS folded the threshold into the
+    // accumulator (bit = sign ^ le), otherwise the (mul, add) table
+    auto epi_word = [&](const uint32_t (&v)[32], int ch) -> uint32_t {
+      if constexpr (BIAS)
+        return sign_word(v) ^ sgm[ch];
+      else
+        return thr_word<true>(v, sthr + ch * 16);
+    };
     int acc = 0;
     uint32_t aph = 0;
     uint32_t it = 0;  // tiles done by this CTA (ALIGN pool buffer parity)
@@ -776,7 +895,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         tmem_wait_ld();
         release_acc(acc);
 #pragma unroll
-        for (int c = 0; c < ECH; ++c) words[c] = thr_word<true>(v[c], sthr + (c0 + c) * 16);
+        for (int c = 0; c < ECH; ++c) words[c] = epi_word(v[c], (c0 + c));
       } else if constexpr (ECH == 4 && PR_ACC == 1 && B2_TMEM_STAGE) {
         // the single 256-column accumulator (BNT = 256): stage the first two
         // chunks in spare TMEM columns (past the accumulator and the scale
@@ -796,13 +915,13 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         tmem_ld32(ta + 96, vb);
         tmem_wait_ld();
         release_acc(acc);
-        words[2] = thr_word<true>(va, sthr + (c0 + 2) * 16);
-        words[3] = thr_word<true>(vb, sthr + (c0 + 3) * 16);
+        words[2] = epi_word(va, (c0 + 2));
+        words[3] = epi_word(vb, (c0 + 3));
         tmem_ld32(spare, va);
         tmem_ld32(spare + 32, vb);
         tmem_wait_ld();
-        words[0] = thr_word<true>(va, sthr + c0 * 16);
-        words[1] = thr_word<true>(vb, sthr + (c0 + 1) * 16);
+        words[0] = epi_word(va, c0);
+        words[1] = epi_word(vb, (c0 + 1));
       } else {
       // software-pipelined: chunk c + 1 is in flight while chunk c is thresholded
       uint32_t va[32], vb[32];
@@ -813,7 +932,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         uint32_t(&v)[32] = (c & 1) ? vb : va;
         uint32_t(&vn)[32] = (c & 1) ? va : vb;
         if (c + 1 < ECH) tmem_ld32(ta + (c + 1) * 32, vn);
-        words[c] = thr_word<true>(v, sthr + (c0 + c) * 16);
+        words[c] = epi_word(v, (c0 + c));
         if (c + 1 < ECH) tmem_wait_ld();
         if (c + 2 == ECH) {  // every chunk is in registers: return the accumulator before the last one's math
           release_acc(acc);
@@ -841,10 +960,10 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
           epi_bar<PR_NEPI>();
           const int ty = r >> g.wshift, x = r & ((1 << g.wshift) - 1);
           if (tv && !(ty & 1) && !(x & 1)) {
-            const int64_t n = pix / g.HW;
-            const int y = (int)((pix - n * g.HW) >> g.wshift);
+            // a tile is whole row pairs of one image: its pooled sites are
+            // the BM / 4 consecutive sites from t BM / 4
             const int wp = (1 << g.wshift) >> 1;
-            uint32_t* o = g.out_bits + ((n * (g.H >> 1) + (y >> 1)) * wp + (x >> 1)) * g.ldo32;
+            uint32_t* o = g.out_bits + (t * (BM / 4) + (ty >> 1) * wp + (x >> 1)) * g.ldo32;
 #pragma unroll
             for (int c = 0; c < ECH; ++c) {
               const uint2 a = sp[(c0 + c) * BM + r], b = sp[(c0 + c) * BM + r + (1 << g.wshift)];
@@ -918,7 +1037,7 @@ inline int padrow_smem_bytes(int nkb, int band_bytes, int nbands = pr_bands<BNT>
   return nkb * (pair ? BNT / 2 : BNT) * 128 + nbands * band_bytes + BNT / 2 * 16 + BNT / 8 +
          8 * (1 + 2 * PR_BANDS_MAX + 2 * pr_acc<BNT>()) + 16 + 8 * 128 +  // MMA offset table (<= 128)
          (pool_buf || pair || raw_bytes ? 2 * BM * (BNT / 32) * 8 : 0) + (pair || raw_bytes ? 8 * PR_BANDS_MAX : 0) +
-         (raw_bytes ? 8 * PR_RAW_SLOTS + PR_RAW_SLOTS * raw_bytes : 0) + 1024;
+         (raw_bytes ? 16 * PR_RAW_SLOTS + 16 + PR_RAW_SLOTS * raw_bytes + 16 + 4096 + 128 : 0) + 1024;
 }
 
 // 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for
