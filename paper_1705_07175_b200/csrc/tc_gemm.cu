@@ -249,12 +249,24 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
                      : AM == A_BYTES_TMA ? (192 * 1024) / ((BN + BM) * BKS)
                                          : b_stages<BN, BKS>();
   g.resb = (!KS && g.N <= BN && g.nkb <= b_room && B2_RESIDENT_B) ? 1 : 0;
+  // fp4 packed output: fold the thresholds into one more MMA per tile (the
+  // bias magnitude |T| + 1 <= K + 1 must fit the two-block encoding)
+  static const int kb_env = [] {
+    const char* e = getenv("B2_KBIAS");
+    return e ? atoi(e) : 1;
+  }();
+  g.kbias = (F4 && !KS && (EM == E_PACK || EM == E_POOLPACK) && kb_env &&
+             (int64_t)((g.N + BN - 1) / BN) * BN <= KB_COLS && k <= 5760)
+                ? (int)k
+                : 0;
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, F4 ? kpad / 2 : kpad, BN)) return rc;
-  auto kern = k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4>;
+  constexpr bool KBP = F4 && !KS && (EM == E_PACK || EM == E_POOLPACK);
+  auto kern = KBP && g.kbias ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP>
+                             : k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, false>;
   constexpr int smem = smem_bytes<BN, AM, BKS, F4>();
-  static std::atomic<uint64_t> attr{0};
-  smem_optin(kern, smem, attr);
+  static std::atomic<uint64_t> attr[2];
+  smem_optin(kern, smem, attr[g.kbias ? 1 : 0]);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   CUtensorMap amap_v;  // A_BYTES_TMA: the u8 rows; unused otherwise
   if (amap)

@@ -84,13 +84,32 @@ struct Args {
   const double* scale;
   const double* beta;
   double* out_f64;  // (M, N), leading dimension ldo
+  // fp4 packed-output kernels: > 0 = K of the layer, thresholds folded into
+  // one more MMA per tile (N columns <= KB_COLS, resident bias block); 0 = table
+  int kbias;
 };
+constexpr int KB_COLS = 512;  // bias-fold column limit (its block reuses the threshold table's 16 KB)
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+// 32-bit shared-window address forms (hot loops: no generic -> shared conversion per use)
+__device__ __forceinline__ void mbar_wait_u(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void sts128_u(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -195,6 +214,12 @@ __device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, u
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+#ifndef B2_EPI_ONE_POLLER  // k_tc_gemm epilogue: one warp polls the accumulator barrier, the rest wait on bar.sync
+#define B2_EPI_ONE_POLLER 1
+#endif
+#ifndef B2_CONV_FAST  // lean fp4 conv producer (ConvCursor); 0 = the general ACursor
+#define B2_CONV_FAST 0  // measured slower than the general cursor (conv4 3.92 vs 3.62 ms) for reasons not yet understood
+#endif
 #ifndef B2_TC_WARP_ISSUE
 #define B2_TC_WARP_ISSUE 0  // measured slower on the im2col kernel (conv4 3.65 -> 4.26 ms)
 #endif
@@ -405,6 +430,74 @@ __device__ __forceinline__ void fence_async_smem() {  // generic-proxy smem writ
 __device__ __forceinline__ uint32_t div_magic(uint32_t n, uint64_t magic) {  // n / d, n < 2^16, d < 2^16
   return (uint32_t)(((uint64_t)n * magic) >> 32);
 }
+// Lean conv cursor (fp4, packed-bit input, no split-K, <= 32 window cells):
+// per tile the row's image site pointer and a bit mask of its in-image
+// window cells; per stage 32-bit offset arithmetic only.  The general cursor
+// spent ~250 instructions per (row, stage) on 64-bit addressing, per-fetch
+// cell decoding and tile bookkeeping (ncu: the producers issued 45 % of the
+// im2col kernel's instructions, and the kernel was issue-bound).
+template <bool POOLED, int WS, int WPH>
+struct ConvCursor {
+  int64_t t;
+  int kb;
+  const uint32_t* rowp;  // site (iy0, ix0) of this row's window (may lie outside the image; read only if valid)
+  uint32_t vmask;        // window cells inside the image (0 for rows past M / tiles past the end)
+  int cell, within, dx, off;
+  __device__ __forceinline__ void tile(const Args& g, int64_t mtiles, int64_t tiles, int r, int half) {
+    kb = 0;
+    const int64_t m = (t % mtiles) * BM + r;
+    const bool mok = t < tiles && m < g.M;
+    int64_t img = 0;
+    int oy = 0, ox = 0;
+    if (mok) row_pos<POOLED>(g, m, img, oy, ox);
+    const int iy0 = oy * g.stride - g.pad, ix0 = ox * g.stride - g.pad;
+    vmask = 0;
+    if (mok)
+      for (int dy = 0, c = 0; dy < g.kh; ++dy)
+        for (int dx_ = 0; dx_ < g.kw; ++dx_, ++c)
+          if ((unsigned)(iy0 + dy) < (unsigned)g.H && (unsigned)(ix0 + dx_) < (unsigned)g.W) vmask |= 1u << c;
+    rowp = g.a + ((img * g.H + iy0) * g.W + ix0) * g.sstride;
+    const int w = WPH * half;  // this thread's first K word of stage 0
+    cell = w / g.spw;
+    within = w - cell * g.spw;
+    const int dy = cell / g.kw;
+    dx = cell - dy * g.kw;
+    off = (dy * g.W + dx) * g.sstride;
+  }
+  __device__ __forceinline__ void start(const Args& g, int64_t t0, int64_t mtiles, int64_t tiles, int r, int half) {
+    t = t0;
+    tile(g, mtiles, tiles, r, half);
+  }
+  __device__ __forceinline__ void fetch(uint4& x, bool& ok) const {
+    ok = (vmask >> cell) & 1u;
+    x = ok ? __ldg(reinterpret_cast<const uint4*>(rowp + off + within)) : make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ void advance(const Args& g, int64_t step, int64_t mtiles, int64_t tiles, int r,
+                                          int half) {
+    if (++kb == g.nkb) {
+      t += step;
+      tile(g, mtiles, tiles, r, half);
+      return;
+    }
+    within += WS;
+    while (within >= g.spw) {
+      within -= g.spw;
+      ++cell;
+      if (++dx == g.kw)
+        dx = 0, off += (g.W - g.kw + 1) * g.sstride;
+      else
+        off += g.sstride;
+    }
+  }
+};
+// 32 bits -> 4 words of e2m1 +-1 nibbles (widen_f4's order) with the sign
+// pattern XORed in: 2 instructions per word; c2 = 0xAAAAAAAA for a valid
+// word (x = 0 and c2 = 0 give 0 nibbles)
+__device__ __forceinline__ void widen_f4x(uint32_t x, uint32_t c2, uint32_t* o) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[q] = ((x << (3 - q)) & 0x88888888u) ^ c2;
+}
+
 template <int AM, bool POOLED, int WS, int TW, bool DIRECT = false>  // WS = K words per stage, TW = words per producer thread
 struct ACursor {
   int64_t t;       // work item of the next fetch (tile t / ksp)
@@ -705,7 +798,8 @@ __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncol
       mul = ge ? 1 : -1;
       add = ge ? -th : th;
     }
-    if constexpr (F4) {  // fp32 accumulators: (mul, add) as floats (|add| < 2^24 exact; larger only for sentinels)
+    if (!sthr) {  // bias fold: the direction masks only
+    } else if constexpr (F4) {  // fp32 accumulators: (mul, add) as floats (|add| < 2^24 exact; larger only for sentinels)
       st[2 * j] = __float_as_int((float)mul);
       st[2 * j + 1] = __float_as_int((float)add);
     } else {
@@ -717,6 +811,58 @@ __device__ __forceinline__ void stage_thresholds(const Args& g, int n0, int ncol
   }
 }
 
+// K-major, no swizzle: 8-row x 16-byte core matrices, LBO = K-plane stride, SBO = 128
+__device__ __forceinline__ uint64_t noswz_desc_k(uint32_t saddr, uint32_t kplane_bytes) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((kplane_bytes >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((128u >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+// ---- threshold folded into the GEMM (tc_padrow.cuh BIAS, k_tc_gemm kbias):
+// one more K = 64 MMA per tile adds a per-filter integer bias -T' to every
+// accumulator, so the epilogue only collects sign bits.  A = a constant +1
+// block, B = the filter's 64 bias elements: block 0 (scale 2^5) holds 16 q,
+// block 1 (scale 2^0) the rest r, b = 16 q + r.  T' = T (ge: bit = acc >= T,
+// sign clear) or T + 1 (le: bit = acc <= T, sign set), clamped to +-(K + 1).
+constexpr uint32_t PR_BIAS_SF = 0x7F7F7F84u;  // scale bytes: block 0 2^5, block 1 2^0
+// e2m1 magnitudes of a count of half units (<= 11): up to two codes
+__device__ __forceinline__ void pr_half_units(int h, int& c0, int& c1) {
+  // 0.5 1 1.5 2 3 4 6 -> codes 1..7 = 1 2 3 4 6 8 12 half units
+  static constexpr int8_t a[12] = {0, 1, 2, 3, 4, 4, 5, 5, 6, 6, 6, 6};
+  static constexpr int8_t b[12] = {0, 0, 0, 0, 0, 1, 0, 1, 0, 1, 2, 3};
+  c0 = a[h], c1 = b[h];
+}
+// 32 e2m1 codes (one scale block) summing to sign * h half units, h <= 30 * 12 + 11
+__device__ __forceinline__ uint4 pr_bias_block(int h, bool neg) {
+  uint32_t w[4] = {0, 0, 0, 0};
+  const uint32_t sg = neg ? 8u : 0u;
+  int e = 0;
+  for (; h >= 12; h -= 12, ++e) w[e >> 3] |= (7u | sg) << (4 * (e & 7));
+  int c0, c1;
+  pr_half_units(h, c0, c1);
+  if (c0) w[e >> 3] |= ((uint32_t)c0 | sg) << (4 * (e & 7)), ++e;
+  if (c1) w[e >> 3] |= ((uint32_t)c1 | sg) << (4 * (e & 7)), ++e;
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// the 32 bytes of filter n's threshold block
+__device__ __forceinline__ void pr_bias_bytes(int64_t bias, uint4& blk0, uint4& blk1) {
+  const int64_t q = bias / 16, r = bias - 16 * q;  // |r| < 16
+  blk0 = pr_bias_block((int)(q < 0 ? -q : q), q < 0);        // q half units of 2^5 = 16 q
+  blk1 = pr_bias_block((int)(2 * (r < 0 ? -r : r)), r < 0);  // 2 |r| half units of 2^0 = r
+}
+// sign word of 32 accumulators: bit j = sign bit of v[j]
+__device__ __forceinline__ uint32_t sign_word(const uint32_t (&v)[32]) {
+  uint32_t sg = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) sg = __funnelshift_l(v[j], sg, 1);
+  return __brev(sg);
+}
+
+// bias of filter n for K-element dot products (padding filters: -1 = bit 0 with ge)
+__device__ __forceinline__ int64_t filter_bias(const int32_t* thresh, const uint8_t* ge, int n, int nvalid, int64_t k) {
+  if (n >= nvalid) return -1;
+  const int64_t th = __ldg(thresh + n);
+  const int64_t b = __ldg(ge + n) ? -th : -(th + 1);
+  return b > k + 1 ? k + 1 : (b < -(k + 1) ? -(k + 1) : b);
+}
 // Packed sign word of 32 accumulators: bit j = (v[j] * mul_j + add_j >= 0)
 // with trow = the columns' (mul, add) pairs (sign bits MSB first, reversed).
 // F4: v holds fp32 accumulators and the table float (mul, add); the sign of
@@ -770,7 +916,10 @@ constexpr int num_threads() {
 // quarter, half the columns each: TMEM reads are latency-bound per warp,
 // ~42 B/clk each, so a single-buffered 256-column accumulator drains twice
 // as fast).
-template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4>
+// KB: thresholds folded into one more MMA per tile (Args.kbias = K; packed
+// fp4 output, <= KB_COLS columns): a separate instantiation, so the
+// threshold-table kernels keep their register allocation
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4, bool KB = false>
 __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
                                                                   const __grid_constant__ CUtensorMap amap,
                                                                   const Args g) {
@@ -804,6 +953,9 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   static_assert(F4 ? (A_COL0 + F4_SF_COLS <= 512) : ATMA ? (A_COL0 <= 512) : (A_COL0 + SA * A_STAGE_COLS <= 512),
                 "TMEM budget");
   constexpr uint32_t IDESC = F4 ? idesc_f4(BN) : idesc_i8(BN, AM == A_BYTES || ATMA);
+  constexpr bool BIASK = KB;
+  static_assert(!KB || (F4 && !KS && (EM == E_PACK || EM == E_POOLPACK)), "bias fold: packed fp4 output");
+  static_assert(!BIASK || A_COL0 + 2 * F4_SF_COLS <= (ACC_BUFS == 1 ? 288 : 512), "TMEM: bias scale columns");
   constexpr int B_REGION = ASMEM ? SB * B_STAGE_BYTES : b_stages<BN, BKS>() * B_STAGE_BYTES;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -821,7 +973,15 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   uint64_t* tfull = empty + SA;
   uint64_t* tempty = tfull + ACC_BUFS;
   uint64_t* bres = tempty + ACC_BUFS;  // resident-B load complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+  uint64_t* bbias = bres + 1;          // kbias: the bias block and the +1 block are written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bbias + 1);
+  // kbias: the filters' bias blocks in the threshold table's place (no
+  // swizzle, K-major: plane p = elements 32 p .. 32 p + 31 of every row, rows
+  // 16 B apart, planes KB_COLS * 16 B apart) and a 128-row +1 block after the barriers
+  uint8_t* sbias = reinterpret_cast<uint8_t*>(sthr);
+  uint8_t* sones = reinterpret_cast<uint8_t*>(tmem_slot + 2);
+  sones += (128u - (smem_u32(sones) & 127u)) & 127u;
+  static_assert(KB_COLS * 32 <= THR_COLS * 8, "bias blocks fit the threshold table");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mtiles = (g.M + BM - 1) / BM;
@@ -840,6 +1000,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       mbar_init(&empty[s], 1);
     }
     mbar_init(bres, 1);
+    mbar_init(bbias, 1);
     for (int a = 0; a < ACC_BUFS; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], NEPI);
@@ -862,6 +1023,11 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
 #pragma unroll
       for (int i = 0; i < 16; ++i) ones[i] = 0x7F7F7F7Fu;
       tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + A_COL0, ones);
+      if constexpr (BIASK) {  // the bias blocks' B scales (every lane quarter holds all N rows)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ones[i] = PR_BIAS_SF;
+        tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + A_COL0 + F4_SF_COLS, ones);
+      }
       tmem_wait_st();
     }
     tc_fence_before();
@@ -919,6 +1085,22 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         }
       }
     }
+  } else if (BIASK && warp == 3) {
+    // ------------------------------------------------ kbias: bias blocks + the +1 block, once
+    {
+      const int ncols = ((g.N + BN - 1) / BN) * BN;
+      for (int n = lane; n < ncols; n += 32) {
+        uint4 b0, b1;
+        pr_bias_bytes(filter_bias(g.thresh, g.ge, n, g.N, g.kbias), b0, b1);
+        *reinterpret_cast<uint4*>(sbias + n * 16) = b0;
+        *reinterpret_cast<uint4*>(sbias + KB_COLS * 16 + n * 16) = b1;
+      }
+      for (int i = lane; i < 4096 / 16; i += 32)
+        reinterpret_cast<uint4*>(sones)[i] = make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bbias);
+    }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     // (B2_TC_WARP_ISSUE: the whole warp runs the loop with uniform
@@ -930,6 +1112,9 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       int acc = 0;
       uint32_t aph = 0;
       if (resb) mbar_wait(bres, 0);
+      bool bias_ready = false;
+      const uint64_t ones_desc = BIASK ? noswz_desc_k(smem_u32(sones), 2048) : 0;
+      const uint64_t bias_desc = BIASK ? noswz_desc_k(smem_u32(sbias), KB_COLS * 16) : 0;
 #ifdef B2_TC_TIMING
       long long c_acc = 0, c_full = 0, c_t0 = clock64(), c_x;
 #endif
@@ -984,6 +1169,13 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           if (pr_elect<WI>()) tc_commit(&empty[s]);
           if (++s == SA) s = 0, ph ^= 1;
         }
+        if constexpr (BIASK) {  // + the tile's columns' bias: A = +1 block, B = bias rows n0 ..
+          if (!bias_ready) mbar_wait(bbias, 0), bias_ready = true;
+          const int n0 = (int)((t / ksp) / mtiles) * BN;
+          if (pr_elect<WI>())
+            tc_mma_f4(d, ones_desc, bias_desc + (uint64_t)((n0 * 16) >> 4), IDESC, tmem + A_COL0,
+                      tmem + A_COL0 + F4_SF_COLS, 1u);
+        }
         if (pr_elect<WI>()) tc_commit(&tfull[acc]);
         if (++acc == ACC_BUFS) acc = 0, aph ^= 1;
       }
@@ -1004,6 +1196,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     const int half = HALVES == 1 ? 0 : (warp - 4) >> 2;
     const int r = q * 32 + lane;  // tile row = TMEM lane
     const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / HALVES);
+    constexpr bool CONV_FAST = AM == A_CONV && F4 && !KS && WPH == 4 && B2_CONV_FAST;
     ACursor<AM, POOLED, WS, WPH, F4 && AM == A_CONV> cur;
     cur.start(g, blockIdx.x, mtiles, tiles, r, half, ksp);
     int64_t jobs;
@@ -1134,6 +1327,47 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           }
         }
       }
+    } else if (CONV_FAST && g.kh * g.kw <= 32) {
+      // lean conv producer (ConvCursor): the same ring of PF prefetched
+      // stages, flattened, with 32-bit shared addresses precomputed
+      ConvCursor<POOLED, WS, WPH> cc;
+      cc.start(g, blockIdx.x, mtiles, tiles, r, half);
+      uint4 qx[PF];
+      bool qok[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        cc.fetch(qx[u], qok[u]);
+        cc.advance(g, gridDim.x, mtiles, tiles, r, half);
+      }
+      const uint32_t row0 = smem_u32(sa) + (uint32_t)r * 128u;
+      const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+      uint32_t ck[4];  // this thread's four 16-byte chunks of its 128-byte row (swizzled)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ck[i] = (uint32_t)(((half * 4 + i) ^ (r & 7)) << 4);
+      const int ijobs = (int)jobs;
+      for (int j0 = 0; j0 < ijobs; j0 += PF) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          if (j0 + u < ijobs) {
+            uint32_t v[16];
+            const uint32_t c2 = qok[u] ? 0xAAAAAAAAu : 0u;
+            widen_f4x(qx[u].x, c2, v + 0);
+            widen_f4x(qx[u].y, c2, v + 4);
+            widen_f4x(qx[u].z, c2, v + 8);
+            widen_f4x(qx[u].w, c2, v + 12);
+            cc.fetch(qx[u], qok[u]);
+            cc.advance(g, gridDim.x, mtiles, tiles, r, half);
+            mbar_wait_u(empty0 + 8u * (uint32_t)s, ph ^ 1);
+            const uint32_t row = row0 + (uint32_t)s * (uint32_t)A_STAGE_BYTES;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) sts128_u(row + ck[i], v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_u(full0 + 8u * (uint32_t)s);
+            if (++s == SA) s = 0, ph ^= 1;
+          }
+        }
+      }
     } else {
       // BYTECONV keeps a per-bit validity word per slot; the row and conv
       // modes only a flag (valid rows widen to +/-1, invalid ones to 0)
@@ -1231,9 +1465,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     // when all N columns fit the table, else staged per tile
     const int ncols = ntiles * BN;
     const bool static_thr = ncols <= THR_COLS;
+    constexpr bool kb_on = BIASK;  // bias fold: sign bits, direction masks only
     if constexpr (EM == E_PACK || EM == E_POOLPACK) {
       if (static_thr) {
-        stage_thresholds<F4>(g, 0, ncols, et, 32 * NEPI, lane, sthr, sgm);
+        stage_thresholds<F4>(g, 0, ncols, et, 32 * NEPI, lane, kb_on ? nullptr : sthr, sgm);
         epi_bar<NEPI>();
       }
     }
@@ -1315,6 +1550,12 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       }
 #ifdef B2_EPI_SLEEP
       mbar_wait_sleep(&tfull[acc], aph, B2_EPI_SLEEP);
+#elif B2_EPI_ONE_POLLER
+      // one warp polls the accumulator barrier, the others block on the
+      // epilogue's named barrier (ncu: eight polling warps spent ~25 % of the
+      // im2col kernel's issue slots spinning here)
+      if (warp == EPI0) mbar_wait(&tfull[acc], aph);
+      epi_bar<NEPI>();
 #else
       mbar_wait_nc(&tfull[acc], aph);
 #endif
@@ -1357,7 +1598,11 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             }
           }
         } else {
-          uint32_t w = thr_word<F4>(v, trow + c * 16);
+          uint32_t w;
+          if constexpr (kb_on)
+            w = sign_word(v) ^ sgm[((tcol + ec0) >> 5) + c];
+          else
+            w = thr_word<F4>(v, trow + c * 16);
           if constexpr (EM == E_POOLPACK) w = pool_word(w, sgm[((tcol + ec0) >> 5) + c]);
           words[c] = w;
         }
@@ -1469,7 +1714,7 @@ constexpr int smem_bytes() {
            1024;
   else if constexpr (F4)
     return f4_stages<BN, BKS>() * (BN + BM) * BKS / 2 + THR_COLS * 8 + THR_COLS / 8 +
-           8 * (2 * f4_stages<BN, BKS>() + 7) + 16 + 1024;
+           8 * (2 * f4_stages<BN, BKS>() + 8) + 16 + 128 + 4096 + 1024;  // (+ bbias, the kbias +1 block)
   else
     return b_stages<BN, BKS>() * BN * BKS + THR_COLS * 8 + THR_COLS / 8 + 8 * (2 * a_stages<BN, AM, BKS>() + 7) +
            16 + 1024;

@@ -173,40 +173,6 @@ constexpr int pr_bands() {
 // bias elements: block 0 (scale 2^5) holds 16 q, block 1 (scale 2^0) the rest
 // r, with b = 16 q + r.  T' = T (ge: bit = acc >= T, i.e. sign clear) or
 // T + 1 (le: bit = acc <= T, i.e. sign set), clamped to +-(K + 1).
-constexpr uint32_t PR_BIAS_SF = 0x7F7F7F84u;  // scale bytes: block 0 2^5, block 1 2^0
-// e2m1 magnitudes of a count of half units (<= 11): up to two codes
-__device__ __forceinline__ void pr_half_units(int h, int& c0, int& c1) {
-  // 0.5 1 1.5 2 3 4 6 -> codes 1..7 = 1 2 3 4 6 8 12 half units
-  static constexpr int8_t a[12] = {0, 1, 2, 3, 4, 4, 5, 5, 6, 6, 6, 6};
-  static constexpr int8_t b[12] = {0, 0, 0, 0, 0, 1, 0, 1, 0, 1, 2, 3};
-  c0 = a[h], c1 = b[h];
-}
-// 32 e2m1 codes (one scale block) summing to sign * h half units, h <= 30 * 12 + 11
-__device__ __forceinline__ uint4 pr_bias_block(int h, bool neg) {
-  uint32_t w[4] = {0, 0, 0, 0};
-  const uint32_t sg = neg ? 8u : 0u;
-  int e = 0;
-  for (; h >= 12; h -= 12, ++e) w[e >> 3] |= (7u | sg) << (4 * (e & 7));
-  int c0, c1;
-  pr_half_units(h, c0, c1);
-  if (c0) w[e >> 3] |= ((uint32_t)c0 | sg) << (4 * (e & 7)), ++e;
-  if (c1) w[e >> 3] |= ((uint32_t)c1 | sg) << (4 * (e & 7)), ++e;
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
-// the 32 bytes of filter n's threshold block
-__device__ __forceinline__ void pr_bias_bytes(int64_t bias, uint4& blk0, uint4& blk1) {
-  const int64_t q = bias / 16, r = bias - 16 * q;  // |r| < 16
-  blk0 = pr_bias_block((int)(q < 0 ? -q : q), q < 0);        // q half units of 2^5 = 16 q
-  blk1 = pr_bias_block((int)(2 * (r < 0 ? -r : r)), r < 0);  // 2 |r| half units of 2^0 = r
-}
-// sign word of 32 accumulators: bit j = sign bit of v[j]
-__device__ __forceinline__ uint32_t sign_word(const uint32_t (&v)[32]) {
-  uint32_t sg = 0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) sg = __funnelshift_l(v[j], sg, 1);
-  return __brev(sg);
-}
-
 // TW (row-aligned, BNT = 128, single CTA): the GEMM transposed — D[filter][pixel]
 // = W[filter][k] X[pixel][k] with the weights as the A operand in TMEM (loaded
 // once, columns PR_TW_COL..) and the band as the B operand.  The MMA then reads
@@ -346,12 +312,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       const int a = g.kk >> 8, ch = ((g.kk & 255) >> 1) >> 4;
       const int64_t kmax = g.kk + 1;
       for (int n = lane; n < BN; n += 32) {
-        int64_t b = -1;  // padding filters: bit 0 (ge with sign set)
-        if (n < g.F) {
-          const int64_t th = __ldg(g.thresh + n);
-          b = __ldg(g.ge + n) ? -th : -(th + 1);
-          b = b > kmax ? kmax : (b < -kmax ? -kmax : b);
-        }
+        const int64_t b = filter_bias(g.thresh, g.ge, n, g.F, kmax - 1);
         uint4 b0, b1;
         pr_bias_bytes(b, b0, b1);
         uint8_t* row = sb + a * BNH * 128 + (n >> 3) * 1024 + (n & 7) * 128;
