@@ -238,6 +238,12 @@ static int num_sms() {
   return n;
 }
 
+// the multicast-weights instantiation exists for the bias-folded fp4 conv kernels
+template <bool F4, bool KS, int EM, int AM>
+constexpr bool KBP_MC() {
+  return F4 && !KS && (EM == E_PACK || EM == E_POOLPACK) && AM == A_CONV;
+}
+
 // KS: split-K over thread-block clusters of g.ksplit CTAs (one tile's K
 // splits), one work item per CTA.
 template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4), bool KS = false, bool F4 = false>
@@ -259,14 +265,25 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
              (int64_t)((g.N + BN - 1) / BN) * BN <= KB_COLS && k <= 5760)
                 ? (int)k
                 : 0;
+  // weight stages shared by CTA pairs (TMA multicast): streamed B (not
+  // resident), bias-folded conv kernels, enough tiles for every SM, an even
+  // number of M tiles (a pair's tiles t, t + 1 share their N tile)
+  static const int mc_env = [] {
+    const char* e = getenv("B2_MCAST");
+    return e ? atoi(e) : 1;
+  }();
+  const int64_t mt_count = (g.M + BM - 1) / BM;
+  const bool mc = KBP_MC<F4, KS, EM, AM>() && g.kbias && !g.resb && mc_env && mt_count % 2 == 0 &&
+                  mt_count * ((g.N + BN - 1) / BN) >= num_sms() && num_sms() % 2 == 0;
   CUtensorMap map;
-  if (int rc = make_bmap(&map, b_i8, g.N, F4 ? kpad / 2 : kpad, BN)) return rc;
+  if (int rc = make_bmap(&map, b_i8, g.N, F4 ? kpad / 2 : kpad, mc ? BN / 2 : BN)) return rc;
   constexpr bool KBP = F4 && !KS && (EM == E_PACK || EM == E_POOLPACK);
-  auto kern = KBP && g.kbias ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP>
+  auto kern = mc            ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, KBP_MC<F4, KS, EM, AM>()>
+              : KBP && g.kbias ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP>
                              : k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, false>;
   constexpr int smem = smem_bytes<BN, AM, BKS, F4>();
-  static std::atomic<uint64_t> attr[2];
-  smem_optin(kern, smem, attr[g.kbias ? 1 : 0]);
+  static std::atomic<uint64_t> attr[3];
+  smem_optin(kern, smem, attr[mc ? 2 : g.kbias ? 1 : 0]);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   CUtensorMap amap_v;  // A_BYTES_TMA: the u8 rows; unused otherwise
   if (amap)
@@ -278,7 +295,10 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   } else {
     g.ksplit = 1;
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    launch_k(kern, grid, num_threads<NPW, NEPI>(), smem, st, map, amap_v, g);
+    if (mc)
+      launch_kc(2, kern, (unsigned)grid, num_threads<NPW, NEPI>(), smem, st, map, amap_v, g);
+    else
+      launch_k(kern, grid, num_threads<NPW, NEPI>(), smem, st, map, amap_v, g);
   }
   return launched();
 }

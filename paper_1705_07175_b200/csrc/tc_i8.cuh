@@ -180,6 +180,20 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
   }
 }
 
+// TMA into the same offset of every CTA in `mask` (cluster), completing on each one's barrier
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank_u() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -236,6 +250,14 @@ __device__ __forceinline__ bool pr_elect() {
   }
 }
 
+// MMA completion -> arrive on `bar` in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -919,7 +941,13 @@ constexpr int num_threads() {
 // KB: thresholds folded into one more MMA per tile (Args.kbias = K; packed
 // fp4 output, <= KB_COLS columns): a separate instantiation, so the
 // threshold-table kernels keep their register allocation
-template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4, bool KB = false>
+// MC: the two CTAs of a cluster share each weight (B) stage: each loads half
+// its rows by TMA multicast into both CTAs' shared memory, and both MMAs'
+// commits release the stage in both (conv4-6 stream every B stage once per
+// 128-pixel tile; the three layers sat at 10-12 TB/s of L2->SM weight
+// traffic, the L2's ceiling).  Needs an even grid and an even number of M
+// tiles, so the two CTAs' tile t and t + 1 always share an N tile.
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4, bool KB = false, bool MC = false>
 __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
                                                                   const __grid_constant__ CUtensorMap amap,
                                                                   const Args g) {
@@ -955,6 +983,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   constexpr uint32_t IDESC = F4 ? idesc_f4(BN) : idesc_i8(BN, AM == A_BYTES || ATMA);
   constexpr bool BIASK = KB;
   static_assert(!KB || (F4 && !KS && (EM == E_PACK || EM == E_POOLPACK)), "bias fold: packed fp4 output");
+  static_assert(!MC || (F4 && !KS), "multicast weights: fp4, no split-K");
   static_assert(!BIASK || A_COL0 + 2 * F4_SF_COLS <= (ACC_BUFS == 1 ? 288 : 512), "TMEM: bias scale columns");
   constexpr int B_REGION = ASMEM ? SB * B_STAGE_BYTES : b_stages<BN, BKS>() * B_STAGE_BYTES;
 
@@ -997,7 +1026,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     for (int s = 0; s < SA; ++s) {
       // every A-producer warp (+ the TMA expect_tx arrival; TMA-fed A: that arrival only)
       mbar_init(&full[s], ATMA ? 1 : NPW + (resb ? 0 : 1));
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs release the stage
     }
     mbar_init(bres, 1);
     mbar_init(bbias, 1);
@@ -1014,7 +1043,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (MC)
+    cluster_sync_all();  // the peer's barriers exist before any multicast or remote commit
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if constexpr (F4) {  // unit block scales (e8m0 0x7F = 2^0) for A and B, every lane
@@ -1077,6 +1109,14 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           } else {
             mbar_expect_tx(&full[s], B_STAGE_BYTES);
           }
+          if constexpr (MC) {
+            // this CTA's half of the rows, into both CTAs' stage s
+            const uint32_t rk = cluster_rank_u();
+#pragma unroll
+            for (int at = 0; at < BKS / 256; ++at)
+              tma_load_2d_mc(sb + s * B_STAGE_BYTES + at * BN * BK + rk * (BN / 2) * BK, &bmap, &full[s],
+                             kb * BKS / 2 + at * BK, n0 + (int)rk * (BN / 2), (uint16_t)3);
+          } else
 #pragma unroll
           for (int at = 0; at < (F4 ? BKS / 256 : BKS / BK); ++at)  // one 128-byte-wide box per swizzle atom
             tma_load_2d(sb + s * B_STAGE_BYTES + at * BN * BK, &bmap, &full[s], (F4 ? kb * BKS / 2 : kb * BKS) + at * BK,
@@ -1166,7 +1206,12 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
                 tc_mma_i8(d, a + k * 8, sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC,
                           (kb > kb0 || k) ? 1u : 0u);
           }
-          if (pr_elect<WI>()) tc_commit(&empty[s]);
+          if (pr_elect<WI>()) {
+            if constexpr (MC)
+              tc_commit_mc(&empty[s], (uint16_t)3);
+            else
+              tc_commit(&empty[s]);
+          }
           if (++s == SA) s = 0, ph ^= 1;
         }
         if constexpr (BIASK) {  // + the tile's columns' bias: A = +1 block, B = bias rows n0 ..
@@ -1700,7 +1745,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (MC)
+    cluster_sync_all();  // no CTA leaves while its peer can still multicast into it or commit to its barriers
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));

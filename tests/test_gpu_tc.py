@@ -101,7 +101,11 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
                                                 (8, 191, 128, 64, False, 20),
                                                 # row-aligned padded-row tiles (pool fused): one image per tile
                                                 # at 8x16, four rows at 4x32
-                                                (8, 16, 128, 96, True, 160), (4, 32, 128, 128, False, 160)])
+                                                (8, 16, 128, 96, True, 160), (4, 32, 128, 128, False, 160),
+                                                # >= 148 tiles, even M-tile count: the bias-folded kernel with
+                                                # weight stages multicast to CTA pairs (conv4-conv6 shapes)
+                                                (16, 16, 256, 256, True, 80), (8, 8, 512, 512, True, 160),
+                                                (8, 8, 256, 512, False, 160)])
 def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch, fmt):
     rng = np.random.default_rng(5 + h + c + f)
     xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
