@@ -553,7 +553,15 @@ inline bool padrow_plan(const Args& g, int c, int64_t filters, int64_t k, int64_
   // the band ring shared memory next to the resident weights
   if ((int64_t)p.R8 * (p.P / 4) > 2 * 32 * PR_NPW || (int64_t)p.R8 * 16 * p.P > 128 * 1024) return false;
   p.band_bytes = padrow_band_bytes(p.R8, p.P);
-  return (filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes) : padrow_smem_bytes<128>(p.nkb, p.band_bytes)) <=
+  // threshold folded into one more MMA (tc_padrow.cuh BIAS): its K block may add an atom
+  p.kk = (int)k;
+  p.nkb_ld = p.nkb;
+  if (B2_PR_VBIAS) {
+    p.nkb = (int)((k + 64 + 255) / 256);
+    if (k % 64) return false;
+  }
+  return (filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, pr_bands<256>(), false, false, 0, B2_PR_VBIAS)
+                        : padrow_smem_bytes<128>(p.nkb, p.band_bytes, pr_bands<128>(), false, false, 0, B2_PR_VBIAS)) <=
          227 * 1024;
 }
 
@@ -637,9 +645,10 @@ inline bool padrow_align_plan(const Args& g, int c, int64_t filters, int64_t k, 
   if (g.sstride % 4) return false;  // bulk copies move whole 16-byte pixels
   const int raw = (int)((int64_t)p.Rb * g.sstride * 4);
   for (p.nbands = PR_BANDS_MAX; p.nbands >= min_bands; --p.nbands) {
-    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw)
-           : p.tw        ? padrow_smem_bytes<128>(0, p.band_bytes, p.nbands, pool != 0, false, raw)
-                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw);
+    const bool bias = !p.tw && !p.pair;
+    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw, bias)
+           : p.tw        ? padrow_smem_bytes<128>(0, p.band_bytes, p.nbands, pool != 0, false, raw, false)
+                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw, bias);
     if (smem <= 227 * 1024) return true;
   }
   return false;
@@ -661,7 +670,8 @@ inline int padrow_run(PadArgs& p, const int8_t* w, int64_t b_row_bytes, int pool
   if (BYTEIN && wide) return B2_EINVAL;
   CUtensorMap map;
   if (int rc = make_bmap(&map, w, p.F, b_row_bytes, wide ? 256 : 128)) return rc;
-  const int smem = wide ? padrow_smem_bytes<256>(p.nkb, p.band_bytes) : padrow_smem_bytes<128>(p.nkb, p.band_bytes);
+  const int smem = wide ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, pr_bands<256>(), false, false, 0, !BYTEIN && B2_PR_VBIAS)
+                        : padrow_smem_bytes<128>(p.nkb, p.band_bytes, pr_bands<128>(), false, false, 0, !BYTEIN && B2_PR_VBIAS);
   static const bool generic_only = getenv("B2_PR_GENERIC") && atoi(getenv("B2_PR_GENERIC"));  // test hook
   const bool k3 = !generic_only && p.kh == 3 && p.kmmas == (BYTEIN ? 1 : 2);  // the unrolled 3x3 issue loops
   void (*kern)(CUtensorMap, PadArgs);

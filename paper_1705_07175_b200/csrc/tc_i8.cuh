@@ -228,6 +228,9 @@ __device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, u
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+#ifndef B2_KB_DRAIN2  // bias-folded single-accumulator drain: two loads, words in between (no spare staging)
+#define B2_KB_DRAIN2 1
+#endif
 #ifndef B2_EPI_ONE_POLLER  // k_tc_gemm epilogue: one warp polls the accumulator barrier, the rest wait on bar.sync
 #define B2_EPI_ONE_POLLER 1
 #endif
@@ -1659,7 +1662,21 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       };
       const uint32_t abase = tmem + lane_addr + acc * ACC_COLS;
       uint32_t va[32], vb[32];
-      if constexpr (STAGE_TMEM) {
+      if constexpr (STAGE_TMEM && KB && B2_KB_DRAIN2) {
+        // bias fold: a chunk collapses to its sign word at once, so the drain
+        // is two TMEM round trips with the first pair's words in between
+        tmem_ld32(abase, va);
+        tmem_ld32(abase + 32, vb);
+        tmem_wait_ld();
+        process(va, 0);
+        process(vb, 1);
+        tmem_ld32(abase + 64, va);
+        tmem_ld32(abase + 96, vb);
+        tmem_wait_ld();
+        release();
+        process(va, 2);
+        process(vb, 3);
+      } else if constexpr (STAGE_TMEM) {
         // single 256-column accumulator (its drain stalls the MMA): copy the
         // first two chunks into this warp's spare TMEM columns, load the last
         // two, release — three TMEM round trips instead of four loads

@@ -116,6 +116,12 @@ constexpr int PR_NPW = 8;       // producer warps
 #ifndef B2_PR_NEPI
 #define B2_PR_NEPI 4
 #endif
+#ifndef B2_PR_VBIAS  // virtual-grid kernel: threshold folded into the GEMM too
+#define B2_PR_VBIAS 0  // measured slower on conv3 (1.80 vs 1.66 ms): one more 128-cycle MMA per tile for an epilogue that was not the limit
+#endif
+#ifndef B2_PR_WI_ALL  // virtual-grid kernel: warp-wide MMA issue too
+#define B2_PR_WI_ALL 0
+#endif
 #ifndef B2_PR_WARP_ISSUE
 #define B2_PR_WARP_ISSUE 1
 #endif
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   static_assert(!(ALIGN && BYTEIN), "row-aligned tiles take packed-bit input");
   static_assert(!PAIR || ALIGN, "CTA pairs only on row-aligned tiles");
   static_assert(!TW || (ALIGN && !PAIR && BNT == 128), "TMEM weights: row-aligned single-CTA 128-pixel tiles");
-  constexpr bool BIAS = ALIGN && !PAIR && !TW;  // threshold folded into the GEMM
+  constexpr bool BIAS = !PAIR && !TW && !BYTEIN && (ALIGN || B2_PR_VBIAS);  // threshold folded into the GEMM
   const int PR_BANDS = ALIGN ? g.nbands : pr_bands<BNT>();
   constexpr uint32_t IDESC = PAIR ? idesc_f4_pair(BN) : idesc_f4(BN);
   constexpr int EPI0 = 4 + PR_NPW;
@@ -224,15 +230,15 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   uint64_t* tempty = tfull + PR_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + PR_ACC);
   uint2* soff = reinterpret_cast<uint2*>(tmem_slot + 2);  // per MMA: (A, B) descriptor address offsets (16 B units)
-  uint2* spool = soff + 128;  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND) of horizontal pairs
+  uint64_t* bbias = reinterpret_cast<uint64_t*>(soff + 128);  // BIAS: threshold block written
+  uint8_t* sones = reinterpret_cast<uint8_t*>(bbias + 2);      // BIAS: 128 rows x 64 e2m1 +1 (4 KB, no swizzle)
+  sones += (128u - (smem_u32(sones) & 127u)) & 127u;
+  uint2* spool = reinterpret_cast<uint2*>(sones + (BIAS ? 4096 : 0));  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND)
   uint64_t* pbfull = reinterpret_cast<uint64_t*>(spool + 2 * BM * (BN / 32));  // PAIR, CTA 0: the peer's band is full
   uint64_t* rfull = pbfull + PR_BANDS_MAX;                                       // ALIGN: raw input staging slot landed
   uint64_t* rempty = rfull + PR_RAW_SLOTS;                                       // ALIGN: every producer warp read it
   uint8_t* sraw = reinterpret_cast<uint8_t*>(rempty + PR_RAW_SLOTS);
   sraw += (16u - (smem_u32(sraw) & 15u)) & 15u;
-  uint64_t* bbias = reinterpret_cast<uint64_t*>(sraw + PR_RAW_SLOTS * g.Rb * g.sstride * 4);  // BIAS: block written
-  uint8_t* sones = reinterpret_cast<uint8_t*>(bbias + 2);  // BIAS: 128 rows x 64 e2m1 +1 (4 KB, no swizzle)
-  sones += (128u - (smem_u32(sones) & 127u)) & 127u;
   // ^ ALIGN: PR_RAW_SLOTS x Rb pixels (16-byte aligned bulk-copy targets)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
 
   if (warp == 0) {
     // ------------------------------------------------ weights, once (PAIR: this CTA's half of the filters)
-    const int nkb_ld = ALIGN && g.nkb_ld ? g.nkb_ld : g.nkb;
+    const int nkb_ld = g.nkb_ld ? g.nkb_ld : g.nkb;
     if (lane == 0 && !TW) {
       mbar_expect_tx(bres, (uint32_t)nkb_ld * BNH * 128);
       for (int a = 0; a < nkb_ld; ++a) tma_load_2d(sb + a * BNH * 128, &bmap, bres, a * 128, (int)rank * BNH);
@@ -319,6 +325,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         *reinterpret_cast<uint4*>(row + ((ch ^ (n & 7)) << 4)) = b0;
         *reinterpret_cast<uint4*>(row + (((ch + 1) ^ (n & 7)) << 4)) = b1;
       }
+      for (int i = lane; i < 4096 / 16; i += 32)  // the threshold block's +1 operand
+        reinterpret_cast<uint4*>(sones)[i] = make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(bbias);
@@ -368,7 +376,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     // MMA, and under epilogue load that chain outlasted the 64-cycle MMA
     // (row-aligned kernels; the virtual-grid 256-column conv3 measured slower
     // with it: 1.83 vs 1.69 ms)
-    constexpr bool WI = ALIGN && B2_PR_WARP_ISSUE;
+    constexpr bool WI = (ALIGN || B2_PR_WI_ALL) && B2_PR_WARP_ISSUE;
     if (WI || lane == 0) {
       // descriptor offsets of every MMA of a tile, once: (window cell, K chunk)
       // -> band plane + row shift for A, weight atom + 32-byte step for B
@@ -557,9 +565,6 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       const int wmask = (1 << g.wshift) - 1;
       for (int i = pt; i < PR_BANDS * g.band_bytes / 16; i += 32 * PR_NPW)
         reinterpret_cast<uint4*>(sband)[i] = make_uint4(0, 0, 0, 0);
-      if constexpr (BIAS)  // the threshold block's +1 operand (published with the first band)
-        for (int i = pt; i < 4096 / 16; i += 32 * PR_NPW)
-          reinterpret_cast<uint4*>(sones)[i] = make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u);
       asm volatile("bar.sync 2, %0;" ::"n"(32 * PR_NPW) : "memory");  // the clear lands before any copy row is stored
       // input pixels from the loader warp's staging ring
       const uint32_t raw_bytes = (uint32_t)g.Rb * (uint32_t)g.sstride * 4u;
@@ -991,14 +996,16 @@ __global__ void k_expand_f4_cells(const uint64_t* __restrict__ w, int64_t rows, 
 }
 
 // raw_bytes > 0 (ALIGN): the spool region is always laid out (the staging
-// ring and its barriers follow it)
+// ring and its barriers follow it); bias: the threshold block's barrier and
+// +1 operand (after the MMA offset table)
 template <int BNT>
 inline int padrow_smem_bytes(int nkb, int band_bytes, int nbands = pr_bands<BNT>(), bool pool_buf = false,
-                             bool pair = false, int raw_bytes = 0) {
+                             bool pair = false, int raw_bytes = 0, bool bias = false) {
   return nkb * (pair ? BNT / 2 : BNT) * 128 + nbands * band_bytes + BNT / 2 * 16 + BNT / 8 +
          8 * (1 + 2 * PR_BANDS_MAX + 2 * pr_acc<BNT>()) + 16 + 8 * 128 +  // MMA offset table (<= 128)
+         (bias ? 16 + 128 + 4096 : 0) +
          (pool_buf || pair || raw_bytes ? 2 * BM * (BNT / 32) * 8 : 0) + (pair || raw_bytes ? 8 * PR_BANDS_MAX : 0) +
-         (raw_bytes ? 16 * PR_RAW_SLOTS + 16 + PR_RAW_SLOTS * raw_bytes + 16 + 4096 + 128 : 0) + 1024;
+         (raw_bytes ? 16 * PR_RAW_SLOTS + 16 + PR_RAW_SLOTS * raw_bytes : 0) + 1024;
 }
 
 // 2x2/2 max-pool of thresholded bits: out word = OR of the window's words for
