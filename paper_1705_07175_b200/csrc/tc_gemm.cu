@@ -278,12 +278,21 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, F4 ? kpad / 2 : kpad, mc ? BN / 2 : BN)) return rc;
   constexpr bool KBP = F4 && !KS && (EM == E_PACK || EM == E_POOLPACK);
-  auto kern = mc            ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, KBP_MC<F4, KS, EM, AM>()>
+  // fp4 A ring in TMEM (k_tc_gemm AT): the 256-column bias-folded conv kernels
+  constexpr bool ATP = KBP_MC<F4, KS, EM, AM>() && BN == 256;
+  static const int at_env = [] {
+    const char* e = getenv("B2_F4_ATMEM");
+    return e ? atoi(e) : 1;
+  }();
+  const bool at = ATP && g.kbias && !g.resb && at_env;
+  auto kern = at && mc      ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, ATP, ATP>
+              : at          ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, false, ATP>
+              : mc          ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, KBP_MC<F4, KS, EM, AM>()>
               : KBP && g.kbias ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP>
                              : k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, false>;
-  constexpr int smem = smem_bytes<BN, AM, BKS, F4>();
-  static std::atomic<uint64_t> attr[3];
-  smem_optin(kern, smem, attr[mc ? 2 : g.kbias ? 1 : 0]);
+  const int smem = at ? smem_bytes_at<BN, BKS>() : smem_bytes<BN, AM, BKS, F4>();
+  static std::atomic<uint64_t> attr[5];
+  smem_optin(kern, smem, attr[at ? (mc ? 4 : 3) : mc ? 2 : g.kbias ? 1 : 0]);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   CUtensorMap amap_v;  // A_BYTES_TMA: the u8 rows; unused otherwise
   if (amap)

@@ -253,6 +253,17 @@ __device__ __forceinline__ bool pr_elect() {
   }
 }
 
+// kind::mxf4 with A from TMEM (TS form)
+__device__ __forceinline__ void tc_mma_f4_ts_g(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
 // MMA completion -> arrive on `bar` in every CTA of `mask`
 __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -789,6 +800,11 @@ constexpr int b_stages() {  // 192 KB of shared memory for the B ring
 // element; the ring holds f4_stages() of each in 192 KB.  TMEM holds only
 // accumulators (3 x 128 or 1 x 256 columns) and the unit scale factors.
 template <int BN, int BKS>
+constexpr int at_stages() {  // fp4 with A in TMEM: B stages in 192 KB, A stages in TMEM columns past 288
+  return (192 * 1024) / (BN * BKS / 2) < (512 - BN - 32) / (BKS / 8) ? (192 * 1024) / (BN * BKS / 2)
+                                                                     : (512 - BN - 32) / (BKS / 8);
+}
+template <int BN, int BKS>
 constexpr int f4_stages() {
   return (192 * 1024) / ((BN + BM) * BKS / 2);
 }
@@ -950,12 +966,19 @@ constexpr int num_threads() {
 // 128-pixel tile; the three layers sat at 10-12 TB/s of L2->SM weight
 // traffic, the L2's ceiling).  Needs an even grid and an even number of M
 // tiles, so the two CTAs' tile t and t + 1 always share an N tile.
-template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4, bool KB = false, bool MC = false>
+// AT (fp4, bias-folded, 256 columns): the A ring lives in TMEM (tcgen05.st by
+// the producers, `kind::mxf4` TS MMAs) and shared memory carries only B: per
+// 128 x 256 tile the MMA's shared-memory reads drop from 432 to 288 KB and the
+// producers' 144 KB of A stores leave shared memory — at the full MMA rate the
+// SS form needed ~864 KB per 4,600-cycle tile against 128 B/clk
+template <int BN, int AM, int EM, int NPW, int BKS, int NEPI, bool KS, bool F4, bool KB = false, bool MC = false,
+          bool AT = false>
 __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const __grid_constant__ CUtensorMap bmap,
                                                                   const __grid_constant__ CUtensorMap amap,
                                                                   const Args g) {
   constexpr bool ATMA = AM == A_BYTES_TMA;  // A by TMA into shared memory, no producer warps
-  constexpr bool ASMEM = F4 || ATMA;        // A ring in shared memory
+  static_assert(!AT || (F4 && KB && BN == 256 && !KS && B2_KB_DRAIN2), "TMEM A ring: bias-folded 256-column fp4 kernels");
+  constexpr bool ASMEM = (F4 && !AT) || ATMA;  // A ring in shared memory
   constexpr int WS = BKS / 32;        // K words per stage
   constexpr int HALVES = NPW >= 4 ? NPW / 4 : 1;  // producer warps per lane quarter
   constexpr int WPH = WS / HALVES;    // K words per producer thread per stage
@@ -973,7 +996,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   // full barrier (TMA bytes + producer warps) and one empty barrier (MMA
   // commit): the issuing thread's per-stage waits and commits are serial
   // time the tensor pipe cannot hide at N = 128 (tools/microbench/mma_loop.cu)
-  constexpr int SA = F4     ? f4_stages<BN, BKS>()
+  constexpr int SA = AT     ? at_stages<BN, BKS>()
+                     : F4     ? f4_stages<BN, BKS>()
                      : ATMA ? (192 * 1024) / (B_STAGE_BYTES + A_STAGE_BYTES)
                             : (a_stages<BN, AM, BKS>() < b_stages<BN, BKS>() ? a_stages<BN, AM, BKS>() : b_stages<BN, BKS>());
   constexpr int SB = SA;
@@ -981,6 +1005,9 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   // TMA-fed u8: TMEM holds only accumulators (no scale factors for int8): double-buffered even at 256 columns
   constexpr int ACC_BUFS = F4 ? f4_acc_bufs<BN>() : ATMA ? (BN > 128 ? 2 : 3) : acc_bufs<BN, AM>();
   constexpr int A_COL0 = ACC_BUFS * ACC_COLS;  // i8: A ring; fp4: scale-factor columns
+  constexpr int AR0 = A_COL0 + 2 * F4_SF_COLS;  // AT: the A ring after the scale and bias-scale columns
+  constexpr int AR_STAGE = BKS / 8;             // AT: TMEM columns per stage (8 e2m1 per column)
+  static_assert(!AT || AR0 + SA * AR_STAGE <= 512, "TMEM: accumulator, scales, A ring");
   static_assert(F4 ? (A_COL0 + F4_SF_COLS <= 512) : ATMA ? (A_COL0 <= 512) : (A_COL0 + SA * A_STAGE_COLS <= 512),
                 "TMEM budget");
   constexpr uint32_t IDESC = F4 ? idesc_f4(BN) : idesc_i8(BN, AM == A_BYTES || ATMA);
@@ -988,7 +1015,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   static_assert(!KB || (F4 && !KS && (EM == E_PACK || EM == E_POOLPACK)), "bias fold: packed fp4 output");
   static_assert(!MC || (F4 && !KS), "multicast weights: fp4, no split-K");
   static_assert(!BIASK || A_COL0 + 2 * F4_SF_COLS <= (ACC_BUFS == 1 ? 288 : 512), "TMEM: bias scale columns");
-  constexpr int B_REGION = ASMEM ? SB * B_STAGE_BYTES : b_stages<BN, BKS>() * B_STAGE_BYTES;
+  constexpr int B_REGION = (ASMEM || AT) ? SB * B_STAGE_BYTES : b_stages<BN, BKS>() * B_STAGE_BYTES;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the shared array (an
@@ -1148,7 +1175,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     // ------------------------------------------------ MMA issuer
     // (B2_TC_WARP_ISSUE: the whole warp runs the loop with uniform
     // descriptors, one elected lane issues — see tc_padrow.cuh)
-    constexpr bool WI = B2_TC_WARP_ISSUE != 0;
+    constexpr bool WI = B2_TC_WARP_ISSUE != 0 || AT;  // AT: measured conv4 3.44 -> 3.30 ms with it
     if (WI || lane == 0) {
       int s = 0;
       uint32_t ph = 0;
@@ -1158,6 +1185,11 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       bool bias_ready = false;
       const uint64_t ones_desc = BIASK ? noswz_desc_k(smem_u32(sones), 2048) : 0;
       const uint64_t bias_desc = BIASK ? noswz_desc_k(smem_u32(sbias), KB_COLS * 16) : 0;
+      // warp-uniform TMEM base and B descriptor halves (the start-address
+      // offsets of a stage only touch the descriptor's low word)
+      const uint32_t tm = WI ? __shfl_sync(0xffffffffu, tmem, 0) : tmem;
+      const uint64_t b0desc = sw128_desc(smem_u32(sb));
+      const uint32_t b0_lo = (uint32_t)b0desc, b0_hi = (uint32_t)(b0desc >> 32);
 #ifdef B2_TC_TIMING
       long long c_acc = 0, c_full = 0, c_t0 = clock64(), c_x;
 #endif
@@ -1184,7 +1216,19 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           tc_fence_after();
           const uint32_t bs = smem_u32(sb + (resb ? kb : s) * B_STAGE_BYTES);
           const int kmma = kb + 1 == g.nkb ? g.klast : BKS / KMMA;
-          if constexpr (F4) {
+          if constexpr (AT) {
+            // A from the TMEM ring (8 columns per K=64), B in shared memory
+            const uint32_t blo = b0_lo + (uint32_t)(((resb ? kb : s) * B_STAGE_BYTES) >> 4);
+            const uint32_t dd = tm + acc * ACC_COLS;
+            if (pr_elect<WI>()) {
+#pragma unroll
+              for (int k = 0; k < BKS / 64; ++k)
+                if (k < kmma)
+                  tc_mma_f4_ts_g(dd, tm + AR0 + s * AR_STAGE + k * 8,
+                                 ((uint64_t)b0_hi << 32) | (blo + (uint32_t)(((k >> 2) * BN * BK + (k & 3) * 32) >> 4)),
+                                 IDESC, tm + A_COL0, tm + A_COL0 + 4, (kb > kb0 || k) ? 1u : 0u);
+            }
+          } else if constexpr (F4) {
             // both operands in shared memory: 4 K=64 MMAs per 128-byte swizzle atom
             const uint32_t as = smem_u32(sa + s * A_STAGE_BYTES);
 #pragma unroll
@@ -1244,6 +1288,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     const int half = HALVES == 1 ? 0 : (warp - 4) >> 2;
     const int r = q * 32 + lane;  // tile row = TMEM lane
     const uint32_t st_addr = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + half * (A_STAGE_COLS / HALVES);
+    const uint32_t at_addr = tmem + ((uint32_t)(q * 32) << 16) + AR0 + half * (AR_STAGE / HALVES);  // AT
     constexpr bool CONV_FAST = AM == A_CONV && F4 && !KS && WPH == 4 && B2_CONV_FAST;
     ACursor<AM, POOLED, WS, WPH, F4 && AM == A_CONV> cur;
     cur.start(g, blockIdx.x, mtiles, tiles, r, half, ksp);
@@ -1265,7 +1310,25 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     // conv; only the first word of each producer's share is consumed
     const bool short_k = HALVES == 1 && g.nkb == 1 && g.klast == 1;
     auto publish = [&](int stage, uint32_t (&v)[VW * WPH]) {  // i8: WPH 2/4/8 -> 16/32/64 TMEM columns
-      if constexpr (F4) {
+      if constexpr (AT) {
+        // fp4 A in TMEM: this thread's 4 words = 16 columns (column j = K
+        // elements 8 j .. 8 j + 7) of its lane, published one stage later
+        if (pending >= 0) {
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[pending]);
+        }
+        mbar_wait_nc(&empty[stage], ph ^ 1);
+        tc_fence_after();
+        static_assert(!AT || WPH == 4 || WPH == 2, "AT: 16 or 8 columns per producer thread");
+        if constexpr (WPH == 4)
+          tmem_st16(at_addr + stage * AR_STAGE, *reinterpret_cast<uint32_t(*)[16]>(v));
+        else
+          tmem_st8(at_addr + stage * AR_STAGE, v);
+        pending = stage;
+        return;
+      } else if constexpr (F4) {
         // fp4: this thread's WPH words of the stage are WPH 16-byte chunks of
         // its row in the shared-memory A stage (128-byte swizzle, K-major)
         mbar_wait_nc(&empty[stage], ph ^ 1);
@@ -1772,6 +1835,11 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   }
 }
 
+template <int BN, int BKS>
+constexpr int smem_bytes_at() {  // fp4, A ring in TMEM: B stages only (+ table, barriers, bias extras)
+  return at_stages<BN, BKS>() * BN * BKS / 2 + THR_COLS * 8 + THR_COLS / 8 + 8 * (2 * at_stages<BN, BKS>() + 8) + 16 +
+         128 + 4096 + 1024;
+}
 template <int BN, int AM, int BKS, bool F4 = false>
 constexpr int smem_bytes() {
   if constexpr (AM == A_BYTES_TMA)

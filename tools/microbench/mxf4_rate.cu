@@ -46,7 +46,16 @@ __global__ void k(int iters, long long* clk, float* check) {
   sbase = (sbase + 1023) & ~1023u;
   uint8_t* sgen = sm + (sbase - (uint32_t)__cvta_generic_to_shared(sm));
   // operands: every byte 0x22 (two +1.0 e2m1 nibbles) / int8 +1
-  for (int i = threadIdx.x; i < 64 * 1024; i += blockDim.x) sgen[i] = KIND ? 0x22 : 0x01;
+  // RANDOM_OPS: random +-1 operands (e2m1 0x2 / 0xA nibbles, int8 +-1) instead of all +1
+  for (int i = threadIdx.x; i < 64 * 1024; i += blockDim.x) {
+#ifdef RANDOM_OPS
+    uint32_t h = (uint32_t)i * 2654435761u ^ (blockIdx.x * 40503u);
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    sgen[i] = KIND ? (uint8_t)(((h & 1) ? 0x02 : 0x0A) | ((h & 2) ? 0x20 : 0xA0)) : (uint8_t)((h & 1) ? 0x01 : 0xFF);
+#else
+    sgen[i] = KIND ? 0x22 : 0x01;
+#endif
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         (uint32_t)__cvta_generic_to_shared(&slot)));
