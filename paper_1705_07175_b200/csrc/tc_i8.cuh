@@ -237,6 +237,9 @@ __device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, u
 #ifndef B2_CONV_FAST  // lean fp4 conv producer (ConvCursor); 0 = the general ACursor
 #define B2_CONV_FAST 0  // measured slower than the general cursor (conv4 3.92 vs 3.62 ms) for reasons not yet understood
 #endif
+#ifndef B2_TC_WI_F4  // fp4 shared-memory kernels: warp-wide uniform MMA issue too
+#define B2_TC_WI_F4 1
+#endif
 #ifndef B2_TC_WARP_ISSUE
 #define B2_TC_WARP_ISSUE 0  // measured slower on the im2col kernel (conv4 3.65 -> 4.26 ms)
 #endif
@@ -1175,7 +1178,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     // ------------------------------------------------ MMA issuer
     // (B2_TC_WARP_ISSUE: the whole warp runs the loop with uniform
     // descriptors, one elected lane issues — see tc_padrow.cuh)
-    constexpr bool WI = B2_TC_WARP_ISSUE != 0 || AT;  // AT: measured conv4 3.44 -> 3.30 ms with it
+    constexpr bool WI = B2_TC_WARP_ISSUE != 0 || AT || (F4 && B2_TC_WI_F4);  // AT: measured conv4 3.44 -> 3.30 ms with it
     if (WI || lane == 0) {
       int s = 0;
       uint32_t ph = 0;
@@ -1230,13 +1233,19 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             }
           } else if constexpr (F4) {
             // both operands in shared memory: 4 K=64 MMAs per 128-byte swizzle atom
-            const uint32_t as = smem_u32(sa + s * A_STAGE_BYTES);
+            // (descriptors as uniform (lo + offset, hi), as the AT form)
+            const uint64_t a0desc = sw128_desc(smem_u32(sa));
+            const uint32_t alo = (uint32_t)a0desc + (uint32_t)((s * A_STAGE_BYTES) >> 4), a_hi = (uint32_t)(a0desc >> 32);
+            const uint32_t blo = b0_lo + (uint32_t)(((resb ? kb : s) * B_STAGE_BYTES) >> 4);
+            const uint32_t dd = tm + acc * ACC_COLS;
+            if (pr_elect<WI>()) {
 #pragma unroll
-            for (int k = 0; k < BKS / 64; ++k)
-              if (k < kmma && pr_elect<WI>())
-                tc_mma_f4(d, sw128_desc(as + (k >> 2) * BM * BK + (k & 3) * 32),
-                          sw128_desc(bs + (k >> 2) * BN * BK + (k & 3) * 32), IDESC, tmem + A_COL0,
-                          tmem + A_COL0 + 4, (kb > kb0 || k) ? 1u : 0u);
+              for (int k = 0; k < BKS / 64; ++k)
+                if (k < kmma)
+                  tc_mma_f4(dd, ((uint64_t)a_hi << 32) | (alo + (uint32_t)(((k >> 2) * BM * BK + (k & 3) * 32) >> 4)),
+                            ((uint64_t)b0_hi << 32) | (blo + (uint32_t)(((k >> 2) * BN * BK + (k & 3) * 32) >> 4)),
+                            IDESC, tm + A_COL0, tm + A_COL0 + 4, (kb > kb0 || k) ? 1u : 0u);
+            }
           } else if constexpr (ATMA) {
             // u8 A and s8 B both in shared memory (128-byte swizzle, K-major)
             const uint32_t as = smem_u32(sa + s * A_STAGE_BYTES);
