@@ -258,7 +258,9 @@ int b2_tc_byte_conv_bn_pack(const uint8_t* x, int64_t batch, int h, int w, int c
  *
  * The same operators on tcgen05.mma kind::mxf4: +1 / -1 / 0 are exact e2m1
  * values (0x2 / 0xA / 0x0), the block scales are all 2^0, and the fp32
- * accumulator holds the exact integer dot product (|dot| < 2^24).  Twice the
+ * accumulator holds the exact integer dot product (|dot| < 2^24; the b2_tc4_*
+ * entry points return B2_EINVAL for K > 2^22, the epilogue's exact float ->
+ * int conversion).  Twice the
  * int8 MMA rate and half the operand bytes.  Weights come from
  * b2_expand_f4; each b2_tc4_X takes exactly the arguments of b2_tc_X with
  * its weight pointer in that format.  Results are identical to b2_tc_X. */

@@ -238,6 +238,9 @@ static int num_sms() {
   return n;
 }
 
+#ifndef B2_MC_ROWS  // the int32 row GEMM (bgemm) shares weight stages between CTA pairs too
+#define B2_MC_ROWS 0  // measured no faster (bgemm 8192: 3.79 vs 3.83 P ops/s)
+#endif
 // the multicast-weights instantiation exists for the bias-folded fp4 conv kernels
 template <bool F4, bool KS, int EM, int AM>
 constexpr bool KBP_MC() {
@@ -248,6 +251,9 @@ constexpr bool KBP_MC() {
 // splits), one work item per CTA.
 template <int BN, int AM, int EM, int NPW, int BKS, int NEPI = (BN > 128 ? 8 : 4), bool KS = false, bool F4 = false>
 int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t st, const CUtensorMap* amap = nullptr) {
+  // fp32 accumulators: exact integers below 2^24; the epilogue's float -> int
+  // conversion (acc_int) needs |dot| < 2^22
+  if (F4 && k > (int64_t(1) << 22)) return B2_EINVAL;
   g.nkb = (int)((k + BKS - 1) / BKS);
   g.klast = (int)(((k - 1) % BKS) / (F4 ? 64 : 32) + 1);
   // one N tile whose every K stage fits the B ring space: keep it resident
@@ -273,19 +279,25 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
     return e ? atoi(e) : 1;
   }();
   const int64_t mt_count = (g.M + BM - 1) / BM;
-  const bool mc = KBP_MC<F4, KS, EM, AM>() && g.kbias && !g.resb && mc_env && mt_count % 2 == 0 &&
-                  mt_count * ((g.N + BN - 1) / BN) >= num_sms() && num_sms() % 2 == 0;
+  const bool mc_geom = !g.resb && mc_env && mt_count % 2 == 0 && mt_count * ((g.N + BN - 1) / BN) >= num_sms() &&
+                       num_sms() % 2 == 0;
+  // the int32 row GEMM (bgemm) shares weight stages only with the TMEM A ring below
+  const bool mc = mc_geom && ((KBP_MC<F4, KS, EM, AM>() && g.kbias) ||
+                              (F4 && !KS && BN == 256 && AM == A_ROWS && EM == E_I32 && B2_MC_ROWS));
   CUtensorMap map;
   if (int rc = make_bmap(&map, b_i8, g.N, F4 ? kpad / 2 : kpad, mc ? BN / 2 : BN)) return rc;
   constexpr bool KBP = F4 && !KS && (EM == E_PACK || EM == E_POOLPACK);
   // fp4 A ring in TMEM (k_tc_gemm AT): the 256-column bias-folded conv kernels
-  constexpr bool ATP = KBP_MC<F4, KS, EM, AM>() && BN == 256;
+  constexpr bool ATP = F4 && !KS && BN == 256 &&
+                      ((AM == A_CONV && (EM == E_PACK || EM == E_POOLPACK)) || (AM == A_ROWS && EM == E_I32));
   static const int at_env = [] {
     const char* e = getenv("B2_F4_ATMEM");
     return e ? atoi(e) : 1;
   }();
-  const bool at = ATP && g.kbias && !g.resb && at_env;
-  auto kern = at && mc      ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, ATP, ATP>
+  const bool at = ATP && (g.kbias || EM == E_I32) && !g.resb && at_env;
+  constexpr bool MCP = (KBP_MC<F4, KS, EM, AM>() || (AM == A_ROWS && EM == E_I32)) && ATP;
+  if (mc && !at && AM == A_ROWS) return B2_EINVAL;  // (no shared-memory multicast row GEMM instantiated)
+  auto kern = at && mc      ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, MCP, ATP>
               : at          ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, false, ATP>
               : mc          ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, KBP_MC<F4, KS, EM, AM>()>
               : KBP && g.kbias ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP>
@@ -326,6 +338,7 @@ inline bool pair_on() {
 }
 template <int AM, int EM>
 int launch_pair(Args g, const int8_t* b, int64_t kpad, int64_t k, cudaStream_t st) {
+  if (k > (int64_t(1) << 22)) return B2_EINVAL;  // see launch_bn
   g.nkb = (int)((k + PAIR_BKS - 1) / PAIR_BKS);
   g.klast = (int)(((k - 1) % PAIR_BKS) / 64 + 1);
   g.resb = 0;

@@ -933,7 +933,10 @@ __device__ __forceinline__ uint32_t thr_word(const uint32_t (&v)[32], const int4
 template <bool F4>
 __device__ __forceinline__ int acc_int(uint32_t v) {  // accumulator -> exact integer
   if constexpr (F4)
-    return __float2int_rn(__uint_as_float(v));
+    // |v| < 2^22 (K <= 2^22, the entry points' limit): v + 1.5 * 2^23 holds v
+    // in its low mantissa bits — an FADD and an integer subtract on the full-
+    // rate pipes instead of the quarter-rate F2I
+    return (int)(__float_as_uint(__fadd_rn(__uint_as_float(v), 12582912.0f)) - 0x4B400000u);
   else
     return (int)v;
 }
@@ -980,7 +983,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
                                                                   const __grid_constant__ CUtensorMap amap,
                                                                   const Args g) {
   constexpr bool ATMA = AM == A_BYTES_TMA;  // A by TMA into shared memory, no producer warps
-  static_assert(!AT || (F4 && KB && BN == 256 && !KS && B2_KB_DRAIN2), "TMEM A ring: bias-folded 256-column fp4 kernels");
+  static_assert(!AT || (F4 && (KB || EM == E_I32) && BN == 256 && !KS && B2_KB_DRAIN2),
+                "TMEM A ring: bias-folded packed or int32 256-column fp4 kernels");
   constexpr bool ASMEM = (F4 && !AT) || ATMA;  // A ring in shared memory
   constexpr int WS = BKS / 32;        // K words per stage
   constexpr int HALVES = NPW >= 4 ? NPW / 4 : 1;  // producer warps per lane quarter
@@ -1734,9 +1738,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       };
       const uint32_t abase = tmem + lane_addr + acc * ACC_COLS;
       uint32_t va[32], vb[32];
-      if constexpr (STAGE_TMEM && KB && B2_KB_DRAIN2) {
-        // bias fold: a chunk collapses to its sign word at once, so the drain
-        // is two TMEM round trips with the first pair's words in between
+      if constexpr (STAGE_TMEM && (KB || AT) && B2_KB_DRAIN2) {
+        // bias fold: a chunk collapses to its sign word at once (int32 output
+        // with the A ring in TMEM: the spare columns are the ring), so the
+        // drain is two TMEM round trips with the first pair processed in between
         tmem_ld32(abase, va);
         tmem_ld32(abase + 32, vb);
         tmem_wait_ld();
