@@ -294,7 +294,7 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
     const char* e = getenv("B2_F4_ATMEM");
     return e ? atoi(e) : 1;
   }();
-  const bool at = ATP && (g.kbias || EM == E_I32) && !g.resb && at_env;
+  const bool at = ATP && (g.kbias || AM == A_ROWS) && !g.resb && at_env;
   constexpr bool MCP = (KBP_MC<F4, KS, EM, AM>() || (AM == A_ROWS && EM == E_I32)) && ATP;
   if (mc && !at && AM == A_ROWS) return B2_EINVAL;  // (no shared-memory multicast row GEMM instantiated)
   auto kern = at && mc      ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, MCP, ATP>

@@ -983,8 +983,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
                                                                   const __grid_constant__ CUtensorMap amap,
                                                                   const Args g) {
   constexpr bool ATMA = AM == A_BYTES_TMA;  // A by TMA into shared memory, no producer warps
-  static_assert(!AT || (F4 && (KB || EM == E_I32) && BN == 256 && !KS && B2_KB_DRAIN2),
-                "TMEM A ring: bias-folded packed or int32 256-column fp4 kernels");
+  static_assert(!AT || (F4 && (KB || AM == A_ROWS) && BN == 256 && !KS && B2_KB_DRAIN2),
+                "TMEM A ring: bias-folded conv or row 256-column fp4 kernels");
   constexpr bool ASMEM = (F4 && !AT) || ATMA;  // A ring in shared memory
   constexpr int WS = BKS / 32;        // K words per stage
   constexpr int HALVES = NPW >= 4 ? NPW / 4 : 1;  // producer warps per lane quarter
@@ -1319,6 +1319,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     }
     int s = 0, pending = -1;
     uint32_t ph = 0;
+#ifdef B2_TC_TIMING
+    long long p_wait = 0;
+    const long long p_t0 = clock64();
+#endif
     // every stage feeds exactly one K=32 MMA (K <= 32, one stage): the first
     // conv; only the first word of each producer's share is consumed
     const bool short_k = HALVES == 1 && g.nkb == 1 && g.klast == 1;
@@ -1332,7 +1336,13 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           __syncwarp();
           if (lane == 0) mbar_arrive(&full[pending]);
         }
+#ifdef B2_TC_TIMING
+        const long long pw0 = clock64();
+#endif
         mbar_wait_nc(&empty[stage], ph ^ 1);
+#ifdef B2_TC_TIMING
+        p_wait += clock64() - pw0;
+#endif
         tc_fence_after();
         static_assert(!AT || WPH == 4 || WPH == 2, "AT: 16 or 8 columns per producer thread");
         if constexpr (WPH == 4)
@@ -1452,6 +1462,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
         }
       }
     } else if (CONV_FAST && g.kh * g.kw <= 32) {
+      if constexpr (CONV_FAST) {
       // lean conv producer (ConvCursor): the same ring of PF prefetched
       // stages, flattened, with 32-bit shared addresses precomputed
       ConvCursor<POOLED, WS, WPH> cc;
@@ -1481,6 +1492,11 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             widen_f4x(qx[u].w, c2, v + 12);
             cc.fetch(qx[u], qok[u]);
             cc.advance(g, gridDim.x, mtiles, tiles, r, half);
+            if constexpr (AT) {  // A ring in TMEM: the generic publish (tcgen05.st, published a stage later)
+              publish(s, v);
+              if (++s == SA) s = 0, ph ^= 1;
+              continue;
+            }
             mbar_wait_u(empty0 + 8u * (uint32_t)s, ph ^ 1);
             const uint32_t row = row0 + (uint32_t)s * (uint32_t)A_STAGE_BYTES;
 #pragma unroll
@@ -1491,6 +1507,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
             if (++s == SA) s = 0, ph ^= 1;
           }
         }
+      }
       }
     } else {
       // BYTECONV keeps a per-bit validity word per slot; the row and conv
@@ -1566,6 +1583,10 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[pending]);
     }
+#ifdef B2_TC_TIMING
+    if (blockIdx.x < 1 && lane == 0 && (warp == 4 || warp == 8))
+      printf("producer warp %d: total %lld  wait empty %lld\n", warp, clock64() - p_t0, p_wait);
+#endif
   } else if (warp >= EPI0) {
     // ------------------------------------------------ epilogue
     constexpr int ECOLS = BN / (NEPI / 4);  // columns per epilogue warp
