@@ -656,22 +656,30 @@ inline bool padrow_align_plan(const Args& g, int c, int64_t filters, int64_t k, 
   p.tw = tw_env && !p.pair && filters <= 128 && PR_TW_COL + (k / 8 + 15) / 16 * 16 <= 512 && (!pool || w <= 32) ? 1 : 0;
   // single-CTA weights-in-shared-memory kernels fold the threshold into one
   // more K = 64 MMA (tc_padrow.cuh BIAS): its block may need one more atom,
-  // and the bias (|T| + 1 <= K + 1) must fit the two-block encoding
-  p.kk = (int)k;
-  p.nkb_ld = p.nkb;
-  if (!p.tw && !p.pair) {
-    if (k > 5760 || k % 64) return false;
-    p.nkb = (int)((k + 64 + 255) / 256);
-  }
-  // the producers' input staging ring (PR_RAW_SLOTS bands of raw pixels)
-  if (g.sstride % 4) return false;  // bulk copies move whole 16-byte pixels
-  const int raw = (int)((int64_t)p.Rb * g.sstride * 4);
-  for (p.nbands = PR_BANDS_MAX; p.nbands >= min_bands; --p.nbands) {
-    const bool bias = !p.tw && !p.pair;
-    smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw, bias)
-           : p.tw        ? padrow_smem_bytes<128>(0, p.band_bytes, p.nbands, pool != 0, false, raw, false)
-                         : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, raw, bias);
-    if (smem <= 227 * 1024) return true;
+  // and the bias (|T| + 1 <= K + 1) must fit the two-block encoding.  The
+  // preferred shape (staging ring + folded threshold) falls back to register-
+  // prefetching producers, then to the threshold table, when the resident
+  // weights leave no room (256 filters at K = 1152: 160 KB).
+  static const int nobias_env = [] {  // B2_ALIGN_NOBIAS=1: keep the threshold in the epilogue (A/B runs)
+    const char* e = getenv("B2_ALIGN_NOBIAS");
+    return e ? atoi(e) : 0;
+  }();
+  const bool bias_ok = !p.tw && !p.pair && k <= 5760 && k % 64 == 0 && !nobias_env;
+  const int nkb0 = p.nkb;
+  const int raw = g.sstride % 4 ? 0 : (int)((int64_t)p.Rb * g.sstride * 4);  // bulk copies move whole 16-byte pixels
+  for (int opt = 0; opt < 3; ++opt) {
+    const bool use_raw = opt == 0 && raw > 0, bias = opt < 2 && bias_ok;
+    p.raw = use_raw ? 1 : 0;
+    p.kk = bias ? (int)k : 0;
+    p.nkb_ld = nkb0;
+    p.nkb = bias ? (int)((k + 64 + 255) / 256) : nkb0;
+    for (p.nbands = PR_BANDS_MAX; p.nbands >= min_bands; --p.nbands) {
+      const int rb = use_raw ? raw : 0;
+      smem = filters > 128 ? padrow_smem_bytes<256>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, rb, bias)
+             : p.tw        ? padrow_smem_bytes<128>(0, p.band_bytes, p.nbands, pool != 0, false, rb, false)
+                           : padrow_smem_bytes<128>(p.nkb, p.band_bytes, p.nbands, pool != 0, p.pair, rb, bias);
+      if (smem <= 227 * 1024) return true;
+    }
   }
   return false;
 }

@@ -68,6 +68,7 @@ struct PadArgs {
   int nbands;          // band slots in the ring (<= PR_BANDS_MAX)
   int pool;            // fused 2x2/2 max-pool (OR ge / AND le of thresholded bits)
   int pair;            // CTA-pair launch (PAIR kernel), set by the host plan
+  int raw;             // ALIGN: input rows through the loader warp's staging ring (0: register prefetch)
   // TW (row-aligned, filters on the MMA's M side): the weights live in TMEM,
   // read once from these fp4 rows (wt_words 32-bit words = K / 8 of each
   // row, rows wt_stride words apart)
@@ -233,8 +234,9 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
   uint64_t* bbias = reinterpret_cast<uint64_t*>(soff + 128);  // BIAS: threshold block written
   uint8_t* sones = reinterpret_cast<uint8_t*>(bbias + 2);      // BIAS: 128 rows x 64 e2m1 +1 (4 KB, no swizzle)
   sones += (128u - (smem_u32(sones) & 127u)) & 127u;
-  uint2* spool = reinterpret_cast<uint2*>(sones + (BIAS ? 4096 : 0));  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND)
-  uint64_t* pbfull = reinterpret_cast<uint64_t*>(spool + 2 * BM * (BN / 32));  // PAIR, CTA 0: the peer's band is full
+  const bool bias_on = BIAS && g.kk > 0;  // the plan may leave the threshold in the epilogue (shared memory)
+  uint2* spool = reinterpret_cast<uint2*>(sones + (bias_on ? 4096 : 0));  // ALIGN + pool: [2 tiles][128 rows][BN / 32] (OR, AND)
+  uint64_t* pbfull = reinterpret_cast<uint64_t*>(spool + (g.pool || PAIR ? 2 * BM * (BN / 32) : 0));  // PAIR, CTA 0: the peer's band is full
   uint64_t* rfull = pbfull + PR_BANDS_MAX;                                       // ALIGN: raw input staging slot landed
   uint64_t* rempty = rfull + PR_RAW_SLOTS;                                       // ALIGN: every producer warp read it
   uint8_t* sraw = reinterpret_cast<uint8_t*>(rempty + PR_RAW_SLOTS);
@@ -258,8 +260,8 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       mbar_init(&bempty[b], 1);
       if constexpr (PAIR) mbar_init(&pbfull[b], 1);
     }
-    if constexpr (BIAS) mbar_init(bbias, 1);
-    if constexpr (ALIGN)
+    if (bias_on) mbar_init(bbias, 1);
+    if (ALIGN && g.raw)
       for (int r = 0; r < PR_RAW_SLOTS; ++r) {
         mbar_init(&rfull[r], 1);
         mbar_init(&rempty[r], PR_NPW);
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       mbar_expect_tx(bres, (uint32_t)nkb_ld * BNH * 128);
       for (int a = 0; a < nkb_ld; ++a) tma_load_2d(sb + a * BNH * 128, &bmap, bres, a * 128, (int)rank * BNH);
     }
-    if constexpr (BIAS) {
+    if (bias_on) {
       // each filter's threshold block at K = kk .. kk + 63 of its weight row
       // (128-byte swizzled atoms: 16-byte chunk c of row n at c ^ (n & 7))
       mbar_wait(bres, 0);
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bbias);
     }
-  } else if (ALIGN && warp == 3) {
+  } else if (ALIGN && warp == 3 && g.raw) {
     // ------------------------------------------------ input loader (ALIGN)
     // The tile's input pixels (rows y0 - pad .. y0 + 128/W - 1 + pad of one
     // image, clamped to the image: one contiguous range) arrive by 1-D bulk
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         }
       if constexpr (WI) __syncwarp();
       mbar_wait(bres, 0);
-      if constexpr (BIAS) mbar_wait(bbias, 0);
+      if (bias_on) mbar_wait(bbias, 0);
       const uint64_t ones_desc = noswz_desc(smem_u32(sones), 2048);
       const uint32_t bias_bo = BIAS ? (uint32_t)((g.kk >> 8) * BNH * 128 + ((g.kk & 255) >> 6) * 32) >> 4 : 0u;
       int slot = 0, acc = 0;
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
                         i ? 1u : 0u);
           }
         }
-        if constexpr (BIAS)
+        if (bias_on)
           tc_mma_f4(d, ones_desc, dsc(b_lo + bias_bo, b_hi), IDESC, tm + SF_COL, tm + SF_BIAS, 1u);
         }
 #ifdef B2_PR_TIMING
@@ -566,6 +568,73 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       for (int i = pt; i < PR_BANDS * g.band_bytes / 16; i += 32 * PR_NPW)
         reinterpret_cast<uint4*>(sband)[i] = make_uint4(0, 0, 0, 0);
       asm volatile("bar.sync 2, %0;" ::"n"(32 * PR_NPW) : "memory");  // the clear lands before any copy row is stored
+      if (!g.raw) {
+      // no room for the staging ring (256 filters: 160 KB of weights): each
+      // producer loads the next tile's pixels into registers before storing
+      // the current band (register double buffer)
+      auto load_tile = [&](int64_t t, uint4 (&w)[UMAX], bool (&ok)[UMAX]) {
+        const int64_t n = t / (g.HW / BM);
+        const int y0 = (int)(((t - n * (g.HW / BM)) * BM) >> g.wshift);
+        const uint32_t* img = g.x + n * g.HW * g.sstride;
+#pragma unroll
+        for (int i = 0; i < UMAX; ++i) {
+          const int u = pt + i * 32 * PR_NPW;
+          ok[i] = false;
+          w[i] = make_uint4(0, 0, 0, 0);
+          if (t < tiles && u < units) {
+            const int b = u / groups, grp = u - b * groups;
+            const int y = y0 - g.pad + (b >> g.wshift);
+            if ((unsigned)y < (unsigned)g.H) {
+              ok[i] = true;
+              w[i] = __ldg(reinterpret_cast<const uint4*>(img + ((int64_t)(y << g.wshift) + (b & wmask)) * g.sstride +
+                                                          4 * grp));
+            }
+          }
+        }
+      };
+      int slot = 0;
+      uint32_t ph = 0;
+      uint4 wa[UMAX], wb[UMAX];
+      bool oka[UMAX], okb[UMAX];
+      load_tile(t_first, wa, oka);
+      auto tile = [&](int64_t t, uint4 (&wc)[UMAX], bool (&okc)[UMAX], uint4 (&wn)[UMAX], bool (&okn)[UMAX]) {
+        load_tile(t + t_step, wn, okn);
+        B2_PR_PROD_WAIT(&bempty[slot], ph ^ 1);
+        uint8_t* band = sband + slot * g.band_bytes;
+#pragma unroll
+        for (int i = 0; i < UMAX; ++i) {
+          const int u = pt + i * 32 * PR_NPW;
+          if (u < units) {
+            const int b = u / groups, grp = u - b * groups;
+            const int x = b & wmask;
+            uint32_t o[16];
+            widen_f4(wc[i].x, okc[i], o);
+            widen_f4(wc[i].y, okc[i], o + 4);
+            widen_f4(wc[i].z, okc[i], o + 8);
+            widen_f4(wc[i].w, okc[i], o + 12);
+#pragma unroll 3
+            for (int dx = 0; dx < kwc; ++dx) {
+              const int xp = x - dx + g.pad;
+              if ((unsigned)xp < (unsigned)(wmask + 1)) {
+                uint8_t* row = band + (size_t)(dx * g.P + 4 * grp) * plane_bytes + (size_t)(b - dx + g.pad) * 16;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  *reinterpret_cast<uint4*>(row + (size_t)j * plane_bytes) =
+                      make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+              }
+            }
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bfull[slot]);
+        if (++slot == PR_BANDS) slot = 0, ph ^= 1;
+      };
+      for (int64_t t = t_first; t - rank < tiles; t += 2 * t_step) {
+        tile(t, wa, oka, wb, okb);
+        if (t + t_step - rank < tiles) tile(t + t_step, wb, okb, wa, oka);
+      }
+      } else {
       // input pixels from the loader warp's staging ring
       const uint32_t raw_bytes = (uint32_t)g.Rb * (uint32_t)g.sstride * 4u;
       int slot = 0, rslot = 0;
@@ -656,6 +725,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         printf("producer cta %d t%d: total %lld  wait slot %lld  sync %lld  raw %lld  other %lld\n", blockIdx.x, pt,
                clock64() - p_t0, p_wait, p_sync, p_raw, p_work - p_sync - p_raw);
 #endif
+      }  // g.raw
     } else {
     // each thread owns up to UMAX (band row, 4-word group) units per tile;
     // a tile's loads are issued before waiting for its band slot
@@ -821,7 +891,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
     // sign word of accumulator chunk ch: BIAS folded the threshold into the
     // accumulator (bit = sign ^ le), otherwise the (mul, add) table
     auto epi_word = [&](const uint32_t (&v)[32], int ch) -> uint32_t {
-      if constexpr (BIAS)
+      if (bias_on)
         return sign_word(v) ^ sgm[ch];
       else
         return thr_word<true>(v, sthr + ch * 16);
@@ -995,16 +1065,16 @@ __global__ void k_expand_f4_cells(const uint64_t* __restrict__ w, int64_t rows, 
   out[t] = word;
 }
 
-// raw_bytes > 0 (ALIGN): the spool region is always laid out (the staging
-// ring and its barriers follow it); bias: the threshold block's barrier and
-// +1 operand (after the MMA offset table)
+// raw_bytes > 0 (ALIGN): the staging ring and its barriers (after the pool
+// exchange, which only pooled / pair launches lay out); bias: the threshold
+// block's barrier and +1 operand (after the MMA offset table)
 template <int BNT>
 inline int padrow_smem_bytes(int nkb, int band_bytes, int nbands = pr_bands<BNT>(), bool pool_buf = false,
                              bool pair = false, int raw_bytes = 0, bool bias = false) {
   return nkb * (pair ? BNT / 2 : BNT) * 128 + nbands * band_bytes + BNT / 2 * 16 + BNT / 8 +
          8 * (1 + 2 * PR_BANDS_MAX + 2 * pr_acc<BNT>()) + 16 + 8 * 128 +  // MMA offset table (<= 128)
          (bias ? 16 + 128 + 4096 : 0) +
-         (pool_buf || pair || raw_bytes ? 2 * BM * (BNT / 32) * 8 : 0) + (pair || raw_bytes ? 8 * PR_BANDS_MAX : 0) +
+         (pool_buf || pair ? 2 * BM * (BNT / 32) * 8 : 0) + (pair || raw_bytes ? 8 * PR_BANDS_MAX : 0) +
          (raw_bytes ? 16 * PR_RAW_SLOTS + 16 + PR_RAW_SLOTS * raw_bytes : 0) + 1024;
 }
 

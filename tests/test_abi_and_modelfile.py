@@ -172,15 +172,15 @@ def test_work_per_image():
 # bench batch.  Path choice is host logic: it runs without a GPU.
 CONV_PATHS = [
     # 129-256 filters at K = 1152: 160 KB of resident weights leave no room for the
-    # row-aligned kernel's input staging ring next to two band slots -> virtual grid
-    ((32, 32, 128, 128, 1, 20), 3), ((16, 16, 128, 64, 0, 80), 3), ((16, 16, 128, 256, 0, 80), 2),
+    # row-aligned kernel's input staging ring -> its register-prefetch producers
+    ((32, 32, 128, 128, 1, 20), 3), ((16, 16, 128, 64, 0, 80), 3), ((16, 16, 128, 256, 0, 80), 3),
     ((64, 64, 128, 128, 1, 6), 3), ((8, 16, 128, 96, 1, 160), 3), ((4, 32, 128, 128, 0, 160), 3),
     ((8, 8, 128, 100, 1, 240), 0), ((62, 62, 128, 128, 0, 6), 2),
     ((16, 16, 128, 200, 1, 80), 0), ((16, 64, 128, 200, 1, 20), 0),
     ((8, 190, 128, 64, 0, 20), 2), ((8, 191, 128, 64, 0, 20), 0), ((32, 32, 128, 128, 1, 2), 0),
     ((4, 4, 512, 512, 1, 1), 1), ((8, 8, 512, 200, 0, 3), 1),
     # BCNN conv2..conv6 at 8192 images
-    ((32, 32, 128, 128, 1, 8192), 3), ((16, 16, 128, 256, 0, 8192), 2), ((16, 16, 256, 256, 1, 8192), 0),
+    ((32, 32, 128, 128, 1, 8192), 3), ((16, 16, 128, 256, 0, 8192), 3), ((16, 16, 256, 256, 1, 8192), 0),
     ((8, 8, 256, 512, 0, 8192), 0), ((8, 8, 512, 512, 1, 8192), 0),
 ]
 
