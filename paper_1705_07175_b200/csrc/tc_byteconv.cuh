@@ -52,7 +52,16 @@ struct ByteConvArgs {
   int64_t ldo32;
 };
 
-constexpr int BC_GROUPS = 2;  // producer groups working on alternate tiles (independent barriers and bands)
+#ifndef B2_BC_GROUPS  // producer groups (3: conv1 1.70 -> 1.50 ms; 768 threads, 85 registers)
+#define B2_BC_GROUPS 3
+#endif
+#ifndef B2_BC_ONE_POLLER
+#define B2_BC_ONE_POLLER 0
+#endif
+#ifndef B2_BC_CHAINS
+#define B2_BC_CHAINS 1
+#endif
+constexpr int BC_GROUPS = B2_BC_GROUPS;  // producer groups working on alternate tiles (independent barriers and bands)
 constexpr int BC_NPW = 4 * BC_GROUPS;  // producer warps: per group, one output row per thread
 constexpr int BC_STAGES = 8;  // A stages (4 KB each)
 constexpr int BC_NEPI = 8;    // epilogue warps (two per TMEM lane quarter)
@@ -145,9 +154,21 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
       const uint64_t bdesc = noswz_desc(smem_u32(sbw), BN * 16);
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
+#ifdef B2_TC_TIMING
+      long long c_acc = 0, c_full = 0, c_t0 = clock64(), c_x;
+#endif
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+#ifdef B2_TC_TIMING
+        c_x = clock64();
+#endif
         mbar_wait(&tempty[acc], aph ^ 1);
+#ifdef B2_TC_TIMING
+        c_acc += clock64() - c_x, c_x = clock64();
+#endif
         mbar_wait(&full[s], ph);
+#ifdef B2_TC_TIMING
+        c_full += clock64() - c_x;
+#endif
         tc_fence_after();
         tc_mma_i8_ss(tmem + acc * BN, noswz_desc(smem_u32(sa + s * A_BYTES), BM * 16), bdesc, IDESC, 0u);
         tc_commit(&empty[s]);
@@ -155,6 +176,11 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
         if (++s == BC_STAGES) s = 0, ph ^= 1;
         if (++acc == ACC) acc = 0, aph ^= 1;
       }
+#ifdef B2_TC_TIMING
+      if (blockIdx.x < 2)
+        printf("byteconv cta %d: total %lld  wait acc %lld  wait full %lld  tiles %lld\n", blockIdx.x, clock64() - c_t0,
+               c_acc, c_full, (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+#endif
     }
   } else if (warp >= 4 && warp < EPI0) {
     // ------------------------------------------------ producers
@@ -318,7 +344,12 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
     const int64_t ostep = (int64_t)gridDim.x * BM * g.ldo32;
     const bool full2 = c0 + 2 <= g.ldo32, one = c0 < g.ldo32;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, orow += ostep) {
+#if B2_BC_ONE_POLLER
+      if (warp == EPI0) mbar_wait(&tfull[acc], aph);  // one warp polls, the others block in hardware
+      epi_bar<BC_NEPI>();
+#else
       mbar_wait(&tfull[acc], aph);
+#endif
       tc_fence_after();
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c0 * 32;
       uint32_t words[ECH];
@@ -331,6 +362,10 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
+#if B2_BC_CHAINS == 4
+#pragma unroll
+        for (int c = 0; c < ECH; ++c) words[c] = ~sign_word(v[c]);
+#else
 #pragma unroll
         for (int c = 0; c < ECH; ++c) {
           uint32_t sg = 0;
@@ -338,6 +373,7 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
           for (int j = 0; j < 32; ++j) sg = __funnelshift_l(v[c][j], sg, 1);  // sign bits, column 0 at the MSB
           words[c] = ~__brev(sg);
         }
+#endif
       } else {
         uint32_t va[32], vb[32];
         tmem_ld32(ta, va);
