@@ -61,7 +61,38 @@ struct ByteConvArgs {
 #ifndef B2_BC_CHAINS
 #define B2_BC_CHAINS 1
 #endif
-constexpr int BC_GROUPS = B2_BC_GROUPS;  // producer groups working on alternate tiles (independent barriers and bands)
+constexpr int BC_GROUPS = B2_BC_GROUPS;
+#ifndef B2_BC_PACK16  // epilogue: 16-bit packed TMEM loads + PRMT sign gathering (filters permuted to match)
+#define B2_BC_PACK16 1
+#endif
+// 32 accumulator columns as 16 registers of two int16 halves (column 2j in the
+// low half of register j) — the int32 accumulators here are |d| <= 2 (K + 1)
+__device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+// sign bits of 32 packed columns: PRMT gathers the high bytes of four
+// columns (4i .. 4i + 3) into q_i (signs at bits 7, 15, 23, 31), and
+// (q_i >> (7 - i)) & (0x01010101 << i) puts column 4i + j at bit 8j + i.
+// The B tile's rows are permuted to match (bc_col_filter), so bit f of the
+// word is filter f.
+__device__ __forceinline__ uint32_t sign_word16(const uint32_t (&v)[16]) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t q = __byte_perm(v[2 * i], v[2 * i + 1], 0x7531);
+    w |= (q >> (7 - i)) & (0x01010101u << i);
+  }
+  return w;
+}
+__host__ __device__ constexpr int bc_col_filter(int col) {  // accumulator column -> filter within its 32-chunk
+  return (col & ~31) | (8 * (col & 3) + ((col & 31) >> 2));
+}  // producer groups working on alternate tiles (independent barriers and bands)
 constexpr int BC_NPW = 4 * BC_GROUPS;  // producer warps: per group, one output row per thread
 constexpr int BC_STAGES = 8;  // A stages (4 KB each)
 constexpr int BC_NEPI = 8;    // epilogue warps (two per TMEM lane quarter)
@@ -126,7 +157,10 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
   // there (d = -1: their padding bits come out 0, as the layout requires)
   const int kpos = perm_pos(g.K);
   for (int i = threadIdx.x; i < BN * 32; i += blockDim.x) {
-    const int f = i >> 5, pos = i & 31;
+    const int col = i >> 5, pos = i & 31;
+    // the filter whose dot lands in accumulator column col (permuted for the
+    // packed-16-bit epilogue, which the 128-column tiles use)
+    const int f = (B2_BC_PACK16 && BN / 32 / (BC_NEPI / 4) <= 2) ? bc_col_filter(col) : col;
     int8_t v = (pos == kpos) ? (int8_t)-1 : (int8_t)0;
     if (f < g.F) {
       const bool ge = __ldg(g.ge + f) != 0;
@@ -139,8 +173,8 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
         v = ge ? wv : (int8_t)-wv;
       }
     }
-    // [plane = pos / 16][row f][16 B]
-    sbw[(pos >> 4) * (BN * 16) + f * 16 + (pos & 15)] = (uint8_t)v;
+    // [plane = pos / 16][row col][16 B]
+    sbw[(pos >> 4) * (BN * 16) + col * 16 + (pos & 15)] = (uint8_t)v;
   }
   fence_async_smem();
   tc_fence_before();
@@ -353,7 +387,17 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
       tc_fence_after();
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c0 * 32;
       uint32_t words[ECH];
-      if constexpr (ECH <= 2) {
+      if constexpr (ECH <= 2 && B2_BC_PACK16) {
+        uint32_t v[ECH][16];
+#pragma unroll
+        for (int c = 0; c < ECH; ++c) tmem_ld16x2(ta + c * 32, v[c]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+#pragma unroll
+        for (int c = 0; c < ECH; ++c) words[c] = ~sign_word16(v[c]);  // bit = d >= 0
+      } else if constexpr (ECH <= 2) {
         // both chunks' loads in flight, one wait, then the accumulator is free
         uint32_t v[ECH][32];
 #pragma unroll
