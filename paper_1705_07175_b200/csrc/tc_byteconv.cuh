@@ -52,8 +52,8 @@ struct ByteConvArgs {
   int64_t ldo32;
 };
 
-#ifndef B2_BC_GROUPS  // producer groups (3: conv1 1.70 -> 1.50 ms; 768 threads, 85 registers)
-#define B2_BC_GROUPS 3
+#ifndef B2_BC_GROUPS  // producer groups (2 -> 3 -> 4: conv1 1.70 -> 1.50 -> 1.16 ms with the later epilogue changes; 896 threads)
+#define B2_BC_GROUPS 4
 #endif
 #ifndef B2_BC_ONE_POLLER
 #define B2_BC_ONE_POLLER 0
@@ -184,8 +184,14 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
 
   if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (the whole warp runs the loop on warp-uniform operands, one elected
+    // lane issues: a lone lane-0 issuer spent ~525 cycles per tile around
+    // its single MMA — the MMA thread had become this kernel's limit)
+    {
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       const uint64_t bdesc = noswz_desc(smem_u32(sbw), BN * 16);
+      const uint64_t a0 = noswz_desc(smem_u32(sa), BM * 16);
+      const uint32_t a_lo = (uint32_t)a0, a_hi = (uint32_t)(a0 >> 32);
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
 #ifdef B2_TC_TIMING
@@ -204,14 +210,16 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
         c_full += clock64() - c_x;
 #endif
         tc_fence_after();
-        tc_mma_i8_ss(tmem + acc * BN, noswz_desc(smem_u32(sa + s * A_BYTES), BM * 16), bdesc, IDESC, 0u);
-        tc_commit(&empty[s]);
-        tc_commit(&tfull[acc]);
+        if (pr_elect<true>()) {
+          tc_mma_i8_ss(tm + acc * BN, ((uint64_t)a_hi << 32) | (a_lo + (uint32_t)((s * A_BYTES) >> 4)), bdesc, IDESC, 0u);
+          tc_commit(&empty[s]);
+          tc_commit(&tfull[acc]);
+        }
         if (++s == BC_STAGES) s = 0, ph ^= 1;
         if (++acc == ACC) acc = 0, aph ^= 1;
       }
 #ifdef B2_TC_TIMING
-      if (blockIdx.x < 2)
+      if (blockIdx.x < 2 && lane == 0)
         printf("byteconv cta %d: total %lld  wait acc %lld  wait full %lld  tiles %lld\n", blockIdx.x, clock64() - c_t0,
                c_acc, c_full, (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 #endif
