@@ -117,6 +117,9 @@ constexpr int PR_NPW = 8;       // producer warps
 #ifndef B2_PR_NEPI
 #define B2_PR_NEPI 4
 #endif
+#ifndef B2_PR_DRAIN2  // bias-folded 256-column padded-row kernels: two-round-trip drain
+#define B2_PR_DRAIN2 0  // measured no faster on conv3 (1.62 vs 1.61 ms)
+#endif
 #ifndef B2_PR_VBIAS  // virtual-grid kernel: threshold folded into the GEMM too
 #define B2_PR_VBIAS 0  // measured slower on conv3 (1.80 vs 1.66 ms): one more 128-cycle MMA per tile for an epilogue that was not the limit
 #endif
@@ -932,6 +935,22 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
         release_acc(acc);
 #pragma unroll
         for (int c = 0; c < ECH; ++c) words[c] = epi_word(v[c], (c0 + c));
+      } else if (ECH == 4 && PR_ACC == 1 && bias_on && B2_PR_DRAIN2) {
+        // bias fold: a chunk is its sign word at once, so two TMEM round
+        // trips with the first pair's words in between release the single
+        // 256-column accumulator (conv3's MMA thread waited 29 % for it)
+        uint32_t va[32], vb[32];
+        tmem_ld32(ta, va);
+        tmem_ld32(ta + 32, vb);
+        tmem_wait_ld();
+        words[0] = epi_word(va, c0);
+        words[1] = epi_word(vb, (c0 + 1));
+        tmem_ld32(ta + 64, va);
+        tmem_ld32(ta + 96, vb);
+        tmem_wait_ld();
+        release_acc(acc);
+        words[2] = epi_word(va, (c0 + 2));
+        words[3] = epi_word(vb, (c0 + 3));
       } else if constexpr (ECH == 4 && PR_ACC == 1 && B2_TMEM_STAGE) {
         // the single 256-column accumulator (BNT = 256): stage the first two
         // chunks in spare TMEM columns (past the accumulator and the scale
