@@ -232,7 +232,7 @@ __device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, u
 #define B2_KB_DRAIN2 1
 #endif
 #ifndef B2_EPI_ONE_POLLER  // k_tc_gemm epilogue: one warp polls the accumulator barrier, the rest wait on bar.sync
-#define B2_EPI_ONE_POLLER 1
+#define B2_EPI_ONE_POLLER 0  // with the warp-issued TMEM-ring kernels all-warp polling measured 1-3 % faster (conv6 3.02 -> 2.93 ms)
 #endif
 #ifndef B2_CONV_FAST  // lean fp4 conv producer (ConvCursor); 0 = the general ACursor
 #define B2_CONV_FAST 0  // measured slower than the general cursor (conv4 3.92 vs 3.62 ms) for reasons not yet understood
