@@ -753,12 +753,12 @@ inline int padrow_run(PadArgs& p, const int8_t* w, int64_t b_row_bytes, int pool
 
 // Launch the row-aligned kernel planned by padrow_align_plan (pool fused).
 inline int padrow_align_run(PadArgs& p, int smem, const void* lines, int sstride, const int8_t* w, int64_t b_row_bytes,
-                            const b2_thresh& th, uint64_t* out, cudaStream_t st) {
+                            const b2_thresh& th, uint64_t* out, cudaStream_t st, int64_t ldo32 = 0) {
   p.x = reinterpret_cast<const uint32_t*>(lines);
   p.sstride = sstride;
   p.thresh = th.thresh;
   p.ge = th.ge_dir;
-  p.ldo32 = 2 * wpl64(p.F);
+  p.ldo32 = ldo32 ? ldo32 : 2 * wpl64(p.F);
   p.out_bits = reinterpret_cast<uint32_t*>(out);
   const bool wide = p.F > 128;
   CUtensorMap map;
@@ -914,7 +914,34 @@ int conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, cons
     PadArgs p;
     int smem = 0;
     switch (conv_path_f4(g, c, filters, k, batch, pool, p, smem)) {
-      case PATH_PADROW_ALIGNED: return padrow_align_run(p, smem, lines, g.sstride, w_i8, kpad_f4(k) / 2, th, out, S(stream));
+      case PATH_PADROW_ALIGNED: {
+        // 129-256 filters: two launches of the 128-filter kernel (each its
+        // own 64 of the output's 128-bit words per 128 filters) — triple-
+        // buffered 128-column accumulators instead of one 256-column
+        // accumulator whose drain the MMA thread waited on 29 % of the time
+        static const int split_env = [] {
+          const char* e = getenv("B2_ALIGN_SPLIT");
+          return e ? atoi(e) : 1;
+        }();
+        PadArgs p2;
+        int smem2 = 0;
+        if (filters > 128 && split_env && padrow_align_plan(g, c, 128, k, batch, pool, p2, smem2)) {
+          const int64_t ldo32 = 2 * wpl64(filters);
+          for (int part = 0; part < 2; ++part) {
+            PadArgs ph = p2;
+            ph.F = part ? (int)(filters - 128) : 128;
+            b2_thresh th2 = th;
+            th2.thresh += 128 * part;
+            th2.ge_dir += 128 * part;
+            if (th2.thresh64) th2.thresh64 += 128 * part;
+            if (int rc = padrow_align_run(ph, smem2, lines, g.sstride, w_i8 + 128 * part * (kpad_f4(k) / 2), kpad_f4(k) / 2,
+                                          th2, out + 2 * part, S(stream), ldo32))
+              return rc;
+          }
+          return 0;
+        }
+        return padrow_align_run(p, smem, lines, g.sstride, w_i8, kpad_f4(k) / 2, th, out, S(stream));
+      }
       case PATH_PADROW: return padrow_launch(p, g, lines, w_i8, k, out, S(stream));
       default: break;
     }
