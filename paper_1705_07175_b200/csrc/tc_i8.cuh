@@ -47,7 +47,10 @@ namespace tc {
 constexpr int BM = 128;                 // tile rows = TMEM lanes
 constexpr int BK = 128;                 // int8 K of one 128-byte swizzle atom (a TMA box row)
 constexpr int KPAD = 512;               // weight rows are padded to a multiple of the widest stage
-constexpr int PF = 4;                   // A-producer prefetch depth (K blocks)
+#ifndef B2_PF
+#define B2_PF 3  // 3: conv4-6 5-8 % faster than 4 (6: slower; 1-2: between)
+#endif
+constexpr int PF = B2_PF;                // A-producer prefetch depth (K blocks)
 
 // A operand sources: packed rows; implicit bit-im2col of NHWC-bits
 // activations; raw u8 rows; masked window rows of the byte-input first conv
