@@ -289,7 +289,8 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   constexpr bool KBP = F4 && !KS && (EM == E_PACK || EM == E_POOLPACK);
   // fp4 A ring in TMEM (k_tc_gemm AT): the 256-column bias-folded conv kernels
   constexpr bool ATP = F4 && !KS && BN == 256 &&
-                      ((AM == A_CONV && (EM == E_PACK || EM == E_POOLPACK)) || (AM == A_ROWS && EM == E_I32));
+                      ((AM == A_CONV && (EM == E_PACK || EM == E_POOLPACK)) ||
+                       (AM == A_ROWS && (EM == E_I32 || EM == E_PACK)));
   static const int at_env = [] {
     const char* e = getenv("B2_F4_ATMEM");
     return e ? atoi(e) : 1;
@@ -297,14 +298,17 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   const bool at = ATP && (g.kbias || AM == A_ROWS) && !g.resb && at_env;
   constexpr bool MCP = (KBP_MC<F4, KS, EM, AM>() || (AM == A_ROWS && EM == E_I32)) && ATP;
   if (mc && !at && AM == A_ROWS) return B2_EINVAL;  // (no shared-memory multicast row GEMM instantiated)
+  // (the KB instantiation only with the bias block actually folded: its
+  // writer fills KB_COLS columns, a wider N would overrun the block)
   auto kern = at && mc      ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, MCP, ATP>
-              : at          ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, false, ATP>
+              : at && g.kbias ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, false, ATP>
+              : at          ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, false, false, (ATP && AM == A_ROWS)>
               : mc          ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP, KBP_MC<F4, KS, EM, AM>()>
               : KBP && g.kbias ? k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, KBP>
                              : k_tc_gemm<BN, AM, EM, NPW, BKS, NEPI, KS, F4, false>;
   const int smem = at ? smem_bytes_at<BN, BKS>() : smem_bytes<BN, AM, BKS, F4>();
-  static std::atomic<uint64_t> attr[5];
-  smem_optin(kern, smem, attr[at ? (mc ? 4 : 3) : mc ? 2 : g.kbias ? 1 : 0]);
+  static std::atomic<uint64_t> attr[6];  // one opt-in record per kernel instantiation chosen above
+  smem_optin(kern, smem, attr[at ? (mc ? 4 : g.kbias ? 3 : 5) : mc ? 2 : g.kbias ? 1 : 0]);
   int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   CUtensorMap amap_v;  // A_BYTES_TMA: the u8 rows; unused otherwise
   if (amap)

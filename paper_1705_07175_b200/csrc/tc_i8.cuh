@@ -47,6 +47,9 @@ namespace tc {
 constexpr int BM = 128;                 // tile rows = TMEM lanes
 constexpr int BK = 128;                 // int8 K of one 128-byte swizzle atom (a TMA box row)
 constexpr int KPAD = 512;               // weight rows are padded to a multiple of the widest stage
+#ifndef B2_AT_STAGES  // TMEM-A-ring kernels: K stages in flight (0 = as many as fit)
+#define B2_AT_STAGES 0
+#endif
 #ifndef B2_PF
 #define B2_PF 3  // 3: conv4-6 5-8 % faster than 4 (6: slower; 1-2: between)
 #endif
@@ -807,8 +810,9 @@ constexpr int b_stages() {  // 192 KB of shared memory for the B ring
 // accumulators (3 x 128 or 1 x 256 columns) and the unit scale factors.
 template <int BN, int BKS>
 constexpr int at_stages() {  // fp4 with A in TMEM: B stages in 192 KB, A stages in TMEM columns past 288
-  return (192 * 1024) / (BN * BKS / 2) < (512 - BN - 32) / (BKS / 8) ? (192 * 1024) / (BN * BKS / 2)
-                                                                     : (512 - BN - 32) / (BKS / 8);
+  constexpr int n = (192 * 1024) / (BN * BKS / 2) < (512 - BN - 32) / (BKS / 8) ? (192 * 1024) / (BN * BKS / 2)
+                                                                               : (512 - BN - 32) / (BKS / 8);
+  return B2_AT_STAGES > 0 && B2_AT_STAGES < n ? B2_AT_STAGES : n;
 }
 template <int BN, int BKS>
 constexpr int f4_stages() {
