@@ -134,7 +134,10 @@ constexpr int PR_BANDS = 4;     // band ring (tiles in flight: hides the band lo
 constexpr int PR_ACC = 3;       // accumulator buffers (3 x 128 columns + scale columns)
 constexpr int PR_BAND_MAX = 16 * 1024;  // bytes per band slot (the minimum; wider images take larger slots)
 constexpr int PR_BANDS_MAX = 4;         // barrier slots reserved for the band ring
-constexpr int PR_RAW_SLOTS = 4;         // ALIGN: raw input staging slots (bulk copies 3 tiles ahead)
+#ifndef B2_PR_RAW_SLOTS
+#define B2_PR_RAW_SLOTS 4
+#endif
+constexpr int PR_RAW_SLOTS = B2_PR_RAW_SLOTS;  // ALIGN: raw input staging slots (bulk copies up to this many tiles ahead)
 
 // 1-D bulk copy global -> shared, completion (bytes) on `bar` (16-byte
 // aligned addresses and size)
