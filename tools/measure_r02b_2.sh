@@ -9,8 +9,8 @@ cap() {  # name, kernel regex, skip, stage
   rm -f gpurun_out/m3_$1_full.ncu-rep
 }
 cap conv1 k_byteconv 1 0
-cap conv2 k_padrow 2 1
-cap conv3 k_padrow 2 2
+cap conv2 k_padrow 3 1
+cap conv3 k_padrow 3 2
 cap conv4 k_tc_gemm 6 3
 cap conv6 k_tc_gemm 6 5
 ls -la gpurun_out
