@@ -820,11 +820,22 @@ inline int padrow_launch(PadArgs& p, const Args& g, const void* lines, const int
 // Kernel choice of the fused fp4 conv (b2_tc4_conv_bn_pack), also exported
 // as b2_tc4_conv_path so tests can assert which kernel a case exercised.
 enum ConvPath { PATH_IM2COL = 0, PATH_SPLITK = 1, PATH_PADROW = 2, PATH_PADROW_ALIGNED = 3 };
+inline bool align_split_on() {  // B2_ALIGN_SPLIT=0: 129-256 filters in one 256-column launch
+  static const int on = [] {
+    const char* e = getenv("B2_ALIGN_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
 inline int conv_path_f4(const Args& g, int c, int64_t filters, int64_t k, int64_t batch, int pool, PadArgs& p,
                         int& smem) {
   if (!batch) return PATH_IM2COL;
   if (splitk_count<A_CONV, E_PACK>(g, k)) return PATH_SPLITK;
   if (padrow_align_plan(g, c, filters, k, batch, pool, p, smem)) return PATH_PADROW_ALIGNED;
+  // 129-256 filters whose 256-column form does not fit (pooled): two
+  // 128-filter launches (conv_bn_pack splits every aligned layer this wide)
+  if (filters > 128 && filters <= 256 && align_split_on() && padrow_align_plan(g, c, 128, k, batch, pool, p, smem))
+    return PATH_PADROW_ALIGNED;
   // pooled layers the row-aligned kernel cannot take use the im2col kernel's
   // fused pool: the virtual grid's pool windows straddle tiles, and an
   // unpooled scratch would be an allocation inside the forward pass
@@ -923,17 +934,14 @@ int conv_bn_pack(const uint64_t* lines, int64_t batch, int h, int w, int c, cons
         // own 64 of the output's 128-bit words per 128 filters) — triple-
         // buffered 128-column accumulators instead of one 256-column
         // accumulator whose drain the MMA thread waited on 29 % of the time
-        static const int split_env = [] {
-          const char* e = getenv("B2_ALIGN_SPLIT");
-          return e ? atoi(e) : 1;
-        }();
         PadArgs p2;
         int smem2 = 0;
-        if (filters > 128 && split_env && padrow_align_plan(g, c, 128, k, batch, pool, p2, smem2)) {
+        if (filters > 128 && align_split_on() && padrow_align_plan(g, c, 128, k, batch, pool, p2, smem2)) {
           const int64_t ldo32 = 2 * wpl64(filters);
           for (int part = 0; part < 2; ++part) {
             PadArgs ph = p2;
             ph.F = part ? (int)(filters - 128) : 128;
+            ph.wlim = (int)(part ? ldo32 - 4 : 4);  // this part's 32-bit words of each pixel
             b2_thresh th2 = th;
             th2.thresh += 128 * part;
             th2.ge_dir += 128 * part;

@@ -69,6 +69,7 @@ struct PadArgs {
   int pool;            // fused 2x2/2 max-pool (OR ge / AND le of thresholded bits)
   int pair;            // CTA-pair launch (PAIR kernel), set by the host plan
   int raw;             // ALIGN: input rows through the loader warp's staging ring (0: register prefetch)
+  int wlim;            // output words this launch writes per pixel (0: ldo32; a filter split's part writes its own)
   // TW (row-aligned, filters on the MMA's M side): the weights live in TMEM,
   // read once from these fp4 rows (wt_words 32-bit words = K / 8 of each
   // row, rows wt_stride words apart)
@@ -819,7 +820,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       add = (float)(ge ? -th : th);
     }
     const uint32_t gm = __ballot_sync(0xffffffffu, ge);  // OR-pool (ge) / AND-pool (le) filters
-    const bool store_q = q < g.ldo32;
+    const bool store_q = q < (g.wlim ? g.wlim : g.ldo32);
     const int wmask = (1 << g.wshift) - 1;
     int acc = 0;
     uint32_t aph = 0;
@@ -894,6 +895,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
       stage_thresholds<true>(ga, 0, BN, et, 32 * PR_NEPI, lane, sthr, sgm);
     }
     epi_bar<PR_NEPI>();
+    const int64_t wlim = g.wlim ? g.wlim : g.ldo32;
     // sign word of accumulator chunk ch: BIAS folded the threshold into the
     // accumulator (bit = sign ^ le), otherwise the (mul, add) table
     auto epi_word = [&](const uint32_t (&v)[32], int ch) -> uint32_t {
@@ -1004,7 +1006,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
           if (tv)
 #pragma unroll
           for (int c = 0; c < ECH; ++c)
-            if (c0 + c < g.ldo32) o[c0 + c] = words[c];
+            if (c0 + c < wlim) o[c0 + c] = words[c];
         } else {
           // 2x2/2 pool inside the tile: OR / AND of the horizontal pair by
           // shuffle, then of the vertical pair (row r + W) through shared
@@ -1026,7 +1028,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
             for (int c = 0; c < ECH; ++c) {
               const uint2 a = sp[(c0 + c) * BM + r], b = sp[(c0 + c) * BM + r + (1 << g.wshift)];
               const uint32_t gm = sgm[c0 + c];
-              if (c0 + c < g.ldo32) o[c0 + c] = ((a.x | b.x) & gm) | ((a.y & b.y) & ~gm);
+              if (c0 + c < wlim) o[c0 + c] = ((a.x | b.x) & gm) | ((a.y & b.y) & ~gm);
             }
           }
         }
@@ -1041,7 +1043,7 @@ __global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
           uint32_t* o = g.out_bits + ((n * g.H + y) * g.W + x) * g.ldo32;
 #pragma unroll
           for (int c = 0; c < ECH; ++c)
-            if (c0 + c < g.ldo32) o[c0 + c] = words[c];
+            if (c0 + c < wlim) o[c0 + c] = words[c];
         }
       }
       }

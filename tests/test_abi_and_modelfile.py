@@ -176,7 +176,7 @@ CONV_PATHS = [
     ((32, 32, 128, 128, 1, 20), 3), ((16, 16, 128, 64, 0, 80), 3), ((16, 16, 128, 256, 0, 80), 3),
     ((64, 64, 128, 128, 1, 6), 3), ((8, 16, 128, 96, 1, 160), 3), ((4, 32, 128, 128, 0, 160), 3),
     ((8, 8, 128, 100, 1, 240), 0), ((62, 62, 128, 128, 0, 6), 2),
-    ((16, 16, 128, 200, 1, 80), 0), ((16, 64, 128, 200, 1, 20), 0),
+    ((16, 16, 128, 200, 1, 80), 3), ((16, 64, 128, 200, 1, 20), 3),
     ((8, 190, 128, 64, 0, 20), 2), ((8, 191, 128, 64, 0, 20), 0), ((32, 32, 128, 128, 1, 2), 0),
     ((4, 4, 512, 512, 1, 1), 1), ((8, 8, 512, 200, 0, 3), 1),
     # BCNN conv2..conv6 at 8192 images

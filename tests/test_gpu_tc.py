@@ -105,7 +105,11 @@ def test_tc_conv_forward_vs_oracle(oracle, h, w, c, f, kh, kw, stride, pad, batc
                                                 # >= 148 tiles, even M-tile count: the bias-folded kernel with
                                                 # weight stages multicast to CTA pairs (conv4-conv6 shapes)
                                                 (16, 16, 256, 256, True, 80), (8, 8, 512, 512, True, 160),
-                                                (8, 8, 256, 512, False, 160)])
+                                                (8, 8, 256, 512, False, 160),
+                                                # 129-256 filters as two 128-filter row-aligned launches:
+                                                # ragged, pooled, the 129-filter edge
+                                                (16, 16, 128, 200, False, 80), (16, 16, 128, 256, True, 80),
+                                                (16, 16, 128, 160, True, 80), (16, 16, 128, 129, False, 80)])
 def test_tc_conv_bn_pack_vs_oracle(oracle, h, w, c, f, pool, batch, fmt):
     rng = np.random.default_rng(5 + h + c + f)
     xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
