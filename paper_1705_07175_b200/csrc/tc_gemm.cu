@@ -33,6 +33,9 @@
 #ifndef B2_NEPI_F4_256  // epilogue warps of fp4 256-column tiles (one accumulator: the drain stalls the MMA)
 #define B2_NEPI_F4_256 8
 #endif
+#ifndef B2_NPW_F4_256  // producer warps of the 256-column fp4 kernels
+#define B2_NPW_F4_256 8
+#endif
 #ifndef B2_NEPI_F4_128  // epilogue warps of fp4 128-column dense tiles (MMAs twice as fast: drain faster)
 #define B2_NEPI_F4_128 8
 #endif
@@ -428,7 +431,7 @@ int launch_f4(Args g, const int8_t* b, int64_t kpad, cudaStream_t st, int64_t k)
           if (pair_on() && ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 255) / 256) >= num_sms() / 2)
             return launch_pair<AM, EM>(g, b, kpad, k, st);
         }
-        return launch_bn<256, AM, EM, 8, 256, B2_NEPI_F4_256, false, true>(g, b, kpad, k, st);
+        return launch_bn<256, AM, EM, B2_NPW_F4_256, 256, B2_NEPI_F4_256, false, true>(g, b, kpad, k, st);
       }
       if constexpr (AM == A_ROWS) return launch_bn<128, AM, EM, 8, 512, B2_NEPI_F4_128, false, true>(g, b, kpad, k, st);
       return launch_bn<128, AM, EM, 8, 512, 4, false, true>(g, b, kpad, k, st);
