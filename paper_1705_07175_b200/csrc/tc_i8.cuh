@@ -234,6 +234,12 @@ __device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, u
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+#ifndef B2_H2  // half-ordered MMA issue with per-half accumulator barriers (see k_tc_gemm H2)
+#define B2_H2 0  // measured slower (conv4 3.18-3.34 vs 3.07 ms with blocks of 1-3 stages): off
+#endif
+#ifndef B2_H2_R  // K stages per half-ordered block
+#define B2_H2_R 3
+#endif
 #ifndef B2_KB_DRAIN2  // bias-folded single-accumulator drain: two loads, words in between (no spare staging)
 #define B2_KB_DRAIN2 1
 #endif
@@ -1026,6 +1032,16 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
                 "TMEM budget");
   constexpr uint32_t IDESC = F4 ? idesc_f4(BN) : idesc_i8(BN, AM == A_BYTES || ATMA);
   constexpr bool BIASK = KB;
+  // H2 (TMEM-A-ring bias-folded 256-column kernels): the accumulator's two
+  // 128-column halves get their own full / empty barriers, and each block of
+  // H2_R K stages is issued half 0 first, then half 1 (N = 128 MMAs).  Half 0
+  // completes H2_R stages before the tile does, so its drain overlaps the
+  // last block's half-1 MMAs, and the next tile's first half-0 MMAs give the
+  // epilogue that much time to drain half 1 (one 256-column accumulator:
+  // the MMA thread had waited 17 % of conv4 for it)
+  constexpr bool H2 = AT && KB && B2_H2 && BN == 256;
+  constexpr int NTB = H2 ? 2 : ACC_BUFS;  // accumulator barrier pairs
+  static_assert(!H2 || (NEPI == 8 && ACC_BUFS == 1 && !B2_EPI_ONE_POLLER), "H2: two epilogue warps per lane quarter");
   static_assert(!KB || (F4 && !KS && (EM == E_PACK || EM == E_POOLPACK)), "bias fold: packed fp4 output");
   static_assert(!MC || (F4 && !KS), "multicast weights: fp4, no split-K");
   static_assert(!BIASK || A_COL0 + 2 * F4_SF_COLS <= (ACC_BUFS == 1 ? 288 : 512), "TMEM: bias scale columns");
@@ -1044,8 +1060,8 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
   uint64_t* full = reinterpret_cast<uint64_t*>(sgm + THR_COLS / 32);
   uint64_t* empty = full + SA;
   uint64_t* tfull = empty + SA;
-  uint64_t* tempty = tfull + ACC_BUFS;
-  uint64_t* bres = tempty + ACC_BUFS;  // resident-B load complete
+  uint64_t* tempty = tfull + NTB;
+  uint64_t* bres = tempty + NTB;  // resident-B load complete
   uint64_t* bbias = bres + 1;          // kbias: the bias block and the +1 block are written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bbias + 1);
   // kbias: the filters' bias blocks in the threshold table's place (no
@@ -1074,9 +1090,9 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
     }
     mbar_init(bres, 1);
     mbar_init(bbias, 1);
-    for (int a = 0; a < ACC_BUFS; ++a) {
+    for (int a = 0; a < NTB; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], NEPI);
+      mbar_init(&tempty[a], H2 ? NEPI / 2 : NEPI);  // H2: one barrier pair per 128-column half
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
@@ -1208,6 +1224,79 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       long long c_acc = 0, c_full = 0, c_t0 = clock64(), c_x;
 #endif
       for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+        if constexpr (H2) {
+          // half-ordered blocks of B2_H2_R stages (see H2 above)
+          int kb0, kb1;
+          item_krange(g, ksp, t, kb0, kb1);
+          const int n0 = (int)((t / ksp) / mtiles) * BN;
+          constexpr uint32_t IDESC128 = idesc_f4(128);
+          for (int b = kb0; b < kb1; b += B2_H2_R) {
+            const int nb = kb1 - b < B2_H2_R ? kb1 - b : B2_H2_R;
+            int ss[B2_H2_R];
+#pragma unroll
+            for (int i = 0; i < B2_H2_R; ++i) {
+              if (i < nb) {
+                ss[i] = s;
+#ifdef B2_TC_TIMING
+                c_x = clock64();
+#endif
+                mbar_wait(&full[s], ph);
+#ifdef B2_TC_TIMING
+                c_full += clock64() - c_x;
+#endif
+                if (++s == SA) s = 0, ph ^= 1;
+              }
+            }
+            tc_fence_after();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (b == kb0) {
+#ifdef B2_TC_TIMING
+                c_x = clock64();
+#endif
+                mbar_wait(&tempty[h], aph ^ 1);
+#ifdef B2_TC_TIMING
+                c_acc += clock64() - c_x;
+#endif
+                tc_fence_after();
+              }
+              if (pr_elect<WI>()) {
+#pragma unroll
+                for (int i = 0; i < B2_H2_R; ++i) {
+                  if (i < nb) {
+                    const int kmma = b + i + 1 == g.nkb ? g.klast : BKS / KMMA;
+                    const uint32_t blo = b0_lo + (uint32_t)((ss[i] * B_STAGE_BYTES + h * 128 * BK) >> 4);
+#pragma unroll
+                    for (int k = 0; k < BKS / 64; ++k)
+                      if (k < kmma)
+                        tc_mma_f4_ts_g(tm + h * 128, tm + AR0 + ss[i] * AR_STAGE + k * 8,
+                                       ((uint64_t)b0_hi << 32) |
+                                           (blo + (uint32_t)(((k >> 2) * BN * BK + (k & 3) * 32) >> 4)),
+                                       IDESC128, tm + A_COL0, tm + A_COL0 + 4, (b > kb0 || i || k) ? 1u : 0u);
+                  }
+                }
+                if (b + nb == kb1) {  // the half's threshold block, then its accumulator is done
+                  if (!bias_ready) mbar_wait(bbias, 0), bias_ready = true;
+                  tc_mma_f4(tm + h * 128, ones_desc, bias_desc + (uint64_t)(((n0 + h * 128) * 16) >> 4), IDESC128,
+                            tm + A_COL0, tm + A_COL0 + F4_SF_COLS, 1u);
+                  tc_commit(&tfull[h]);
+                }
+              }
+            }
+            if (pr_elect<WI>()) {
+#pragma unroll
+              for (int i = 0; i < B2_H2_R; ++i)
+                if (i < nb) {
+                  if constexpr (MC)
+                    tc_commit_mc(&empty[ss[i]], (uint16_t)3);
+                  else
+                    tc_commit(&empty[ss[i]]);
+                }
+            }
+          }
+          aph ^= 1;
+          continue;
+        }
 #ifdef B2_TC_TIMING
         c_x = clock64();
 #endif
@@ -1709,7 +1798,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       if (warp == EPI0) mbar_wait(&tfull[acc], aph);
       epi_bar<NEPI>();
 #else
-      mbar_wait_nc(&tfull[acc], aph);
+      mbar_wait_nc(&tfull[H2 ? ((warp - EPI0) >> 2) : acc], aph);
 #endif
       tc_fence_after();
       uint32_t words[ECH];
@@ -1762,7 +1851,7 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
       auto release = [&]() {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) mbar_arrive(&tempty[H2 ? ((warp - EPI0) >> 2) : acc]);
       };
       const uint32_t abase = tmem + lane_addr + acc * ACC_COLS;
       uint32_t va[32], vb[32];
