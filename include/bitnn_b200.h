@@ -289,7 +289,9 @@ int b2_tc4_conv_forward(const uint64_t* lines, int64_t batch, int h, int w, int 
  *    multiple of 128 (pooled: 128 / w even), weights plus >= 2 band slots in
  *    shared memory and >= one 128-pixel tile per SM: the ROW-ALIGNED
  *    padded-row implicit GEMM, pooling fused into its epilogue (DESIGN.md
- *    §3.1b);
+ *    §3.1b); 129-256 filters run as two 128-filter launches (each writes its
+ *    own output words; B2_ALIGN_SPLIT=0 keeps one 256-column launch where it
+ *    fits);
  *  - otherwise unpooled stride-1 same-size convs with c % 128 == 0, <= 256
  *    filters (K <= 1536 up to 128 filters, <= 1280 above), a band the producer
  *    warps cover (c = 128: w <= 190), weights resident, and enough virtual
