@@ -50,6 +50,9 @@ constexpr int KPAD = 512;               // weight rows are padded to a multiple 
 #ifndef B2_AT_STAGES  // TMEM-A-ring kernels: K stages in flight (0 = as many as fit)
 #define B2_AT_STAGES 0
 #endif
+#ifndef B2_AT_EAGER  // TMEM-A-ring producers: publish each stage right after its store drains (1) or a stage later (0)
+#define B2_AT_EAGER 0
+#endif
 #ifndef B2_PF
 #define B2_PF 3  // 3: conv4-6 5-8 % faster than 4 (6: slower; 1-2: between)
 #endif
@@ -1445,6 +1448,13 @@ __global__ void __launch_bounds__(num_threads<NPW, NEPI>(), 1) k_tc_gemm(const _
           tmem_st16(at_addr + stage * AR_STAGE, *reinterpret_cast<uint32_t(*)[16]>(v));
         else
           tmem_st8(at_addr + stage * AR_STAGE, v);
+        if constexpr (B2_AT_EAGER) {  // publish now (the store's drain on this warp's critical path)
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[stage]);
+          return;
+        }
         pending = stage;
         return;
       } else if constexpr (F4) {
