@@ -783,6 +783,17 @@ class Network:
         Staged input: equal chunks that fit half the pinned workspace."""
         if pinned:
             f = self._pipe_split if self._pipe_split is not None else 0.125
+            # chunk i+1's H2D hides under chunk i's pass when c_{i+1} <= r c_i
+            # (r = compute / H2D time per image), so the sizes grow
+            # geometrically and only the first, smallest chunk's H2D is
+            # exposed; three chunks when the first stays >= 2048 images
+            # (two chunks exposed ~5 % of a 65536-image BCNN call)
+            r = (1.0 - f) / max(f, 1e-3)
+            if r > 1.0 and n * 1.0 / (1.0 + r + r * r) >= 2048:
+                c0 = max(512, -(-int(n / (1.0 + r + r * r)) // 512) * 512)
+                c1 = max(512, int(c0 * r) // 512 * 512)
+                if c0 + c1 + 512 <= n:
+                    return [(0, c0), (c0, c1), (c0 + c1, n - c0 - c1)]
             c0 = max(512, -(-int(n * f) // 512) * 512)
             return [(0, c0), (c0, n - c0)] if n - c0 >= 512 else [(0, n)]
         ck = self.cap if self.cap < 2048 else max(1024, self.cap // 4)
