@@ -277,9 +277,11 @@ int launch_bn(Args g, const int8_t* b_i8, int64_t kpad, int64_t k, cudaStream_t 
   // weight stages shared by CTA pairs (TMA multicast): streamed B (not
   // resident), bias-folded conv kernels, enough tiles for every SM, an even
   // number of M tiles (a pair's tiles t, t + 1 share their N tile)
+  // (off by default: with the TMEM A ring and the warp-wide issue it measured
+  // 3-4 % slower on conv4 and equal on conv5/conv6; B2_MCAST=1 opts in)
   static const int mc_env = [] {
     const char* e = getenv("B2_MCAST");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   const int64_t mt_count = (g.M + BM - 1) / BM;
   const bool mc_geom = !g.resb && mc_env && mt_count % 2 == 0 && mt_count * ((g.N + BN - 1) / BN) >= num_sms() &&
