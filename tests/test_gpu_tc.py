@@ -408,6 +408,42 @@ def test_tc_conv_forward_random_geometry(oracle, seed, fmt):
     assert np.array_equal(_dev.download(out, np.int32), want), (h, w, c, f, kh, kw, stride, pad, batch)
 
 
+# random row-aligned padded-row launches (>= one 128-pixel tile per SM): 16x16
+# or 32x32, C = 128, 1-256 filters (the 129-256 split included), pooled or
+# not, BN thresholds with ALWAYS / NEVER sentinels and le filters; checked
+# bit-exact against the oracle and asserted to take the row-aligned path
+@pytest.mark.parametrize("seed", range(12))
+def test_tc_conv_bn_pack_random_aligned(oracle, seed):
+    rng = np.random.default_rng(9000 + seed)
+    h = w = int(rng.choice([16, 32]))
+    c = 128
+    f = int(rng.integers(1, 257))
+    pool = bool(rng.integers(0, 2))
+    batch = 80 if h == 16 else 20
+    if _lib._so.b2_tc4_conv_path(batch, h, w, c, f, 3, 3, 1, 1, int(pool)) != 3:
+        pytest.skip("shape not on the row-aligned path")
+    xs = [oracle.pack_lines(rand_pm1(rng, h * w, c)) for _ in range(batch)]
+    wt = oracle.pack_lines(rand_pm1(rng, f, 9 * c))
+    bn = rand_bn(rng, f, 20.0)
+    bn.gamma[::7] = 0.0
+    bn.gamma[3::11] *= -1
+    bn = BatchNormLayer(bn.mean, bn.var, bn.gamma, bn.beta)
+    corr = oracle.compute_correction(wt, (h, w, c), (3, 3), 1, 1)
+    want = []
+    for x in xs:
+        acc = (oracle.bgemm(oracle.unroll_packed(x, h, w, c, 3, 3, 1, 1), wt, 9 * c) + corr).reshape(h, w, f)
+        if pool:
+            acc = oracle.maxpool(acc, 2, 2, 2)
+        want.append(oracle.threshold_sign_pack(acc.reshape(-1, f), bn.thresh, bn.ge_dir, False))
+    cal = layers.calibrate_device(bn.mean, bn.var, bn.gamma, bn.beta, bn.eps, 9 * c)
+    w8 = _dev.tc_weights(_dev.upload(wt), f, 9 * c, "f4")
+    sites = h * w // (4 if pool else 1)
+    out = _dev.upload(np.full((batch, sites, -(-f // 64)), 0xFFFFFFFFFFFFFFFF, np.uint64))
+    _lib.call(_lib.tc_entry("conv_bn_pack", "f4"), _dev.P(_dev.upload(np.stack(xs))), batch, h, w, c, _dev.P(w8), f,
+              3, 3, 1, 1, int(pool), th(cal), _dev.P(out), _dev.stream())
+    assert np.array_equal(_dev.download(out, np.uint64), np.stack(want)), (h, w, f, pool)
+
+
 @pytest.mark.parametrize("seed", range(20))
 def test_tc_conv_bn_pack_random_geometry(oracle, seed, fmt):
     rng = np.random.default_rng(5000 + seed)
