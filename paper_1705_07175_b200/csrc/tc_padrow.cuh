@@ -118,6 +118,9 @@ constexpr int PR_NPW = 8;       // producer warps
 #ifndef B2_PR_NEPI
 #define B2_PR_NEPI 4
 #endif
+#ifndef B2_PR_NEPI_ALIGN  // epilogue warps of the 128-column row-aligned kernel
+#define B2_PR_NEPI_ALIGN 4  // 4: conv2 / conv3 ~1 % faster than 8
+#endif
 #ifndef B2_PR_DRAIN2  // bias-folded 256-column padded-row kernels: two-round-trip drain
 #define B2_PR_DRAIN2 0  // measured no faster on conv3 (1.62 vs 1.61 ms)
 #endif
@@ -159,7 +162,7 @@ __device__ __forceinline__ void bulk_g2s_pr(void* dst, const void* src, uint32_t
 // epilogue warps, three band slots.
 template <int BNT, bool ALIGN = false>
 constexpr int pr_nepi() {  // row-aligned 128-column tiles: two warps per lane quarter, 64 columns each
-  return BNT == 256 ? 8 : (ALIGN ? 8 : PR_NEPI);
+  return BNT == 256 ? 8 : (ALIGN ? B2_PR_NEPI_ALIGN : PR_NEPI);
 }
 template <int BNT>
 constexpr int pr_acc() {
