@@ -785,7 +785,7 @@ inline int padrow_align_run(PadArgs& p, int smem, const void* lines, int sstride
     static std::atomic<uint64_t> attr3[2];
     smem_optin(kern, 227 * 1024, attr3[k3 ? 1 : 0]);
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    launch_k(kern, grid, threads, smem, st, map, p);
+    launch_k(kern, grid, 32 * (4 + PR_NPW + pr_nepi<128, true, true>()), smem, st, map, p);
     return launched();
   }
   if (p.pair) {

@@ -160,9 +160,9 @@ __device__ __forceinline__ void bulk_g2s_pr(void* dst, const void* src, uint32_t
 // band slots; BNT = 256 (up to 256 filters, weights <= 160 KB): one
 // 256-column accumulator (2 x 256 + the scale columns exceed TMEM), eight
 // epilogue warps, three band slots.
-template <int BNT, bool ALIGN = false>
-constexpr int pr_nepi() {  // row-aligned 128-column tiles: two warps per lane quarter, 64 columns each
-  return BNT == 256 ? 8 : (ALIGN ? B2_PR_NEPI_ALIGN : PR_NEPI);
+template <int BNT, bool ALIGN = false, bool TW = false>
+constexpr int pr_nepi() {  // row-aligned 128-column tiles: B2_PR_NEPI_ALIGN warps (TW: two per lane quarter)
+  return BNT == 256 ? 8 : (TW ? 8 : (ALIGN ? B2_PR_NEPI_ALIGN : PR_NEPI));
 }
 template <int BNT>
 constexpr int pr_acc() {
@@ -211,11 +211,11 @@ __device__ __forceinline__ void tc_mma_f4_ts(uint32_t d_tmem, uint32_t a_tmem, u
 }
 
 template <int KH, int KMMAS, int BNT, bool BYTEIN = false, bool ALIGN = false, bool PAIR = false, bool TW = false>
-__global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN>()), 1)
+__global__ void __launch_bounds__(32 * (4 + PR_NPW + pr_nepi<BNT, ALIGN, TW>()), 1)
     k_padrow_conv(const __grid_constant__ CUtensorMap bmap, const PadArgs g) {
   constexpr int BN = BNT;
   constexpr int BNH = PAIR ? BN / 2 : BN;  // weight rows held by this CTA
-  constexpr int PR_NEPI = pr_nepi<BNT, ALIGN>();
+  constexpr int PR_NEPI = pr_nepi<BNT, ALIGN, TW>();
   constexpr int PR_ACC = TW ? 2 : pr_acc<BNT>();  // TW: 2 x 128 accumulator columns, scales, then the weights
   static_assert(!(ALIGN && BYTEIN), "row-aligned tiles take packed-bit input");
   static_assert(!PAIR || ALIGN, "CTA pairs only on row-aligned tiles");
