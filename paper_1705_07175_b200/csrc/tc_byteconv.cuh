@@ -94,9 +94,15 @@ __host__ __device__ constexpr int bc_col_filter(int col) {  // accumulator colum
   return (col & ~31) | (8 * (col & 3) + ((col & 31) >> 2));
 }  // producer groups working on alternate tiles (independent barriers and bands)
 constexpr int BC_NPW = 4 * BC_GROUPS;  // producer warps: per group, one output row per thread
-constexpr int BC_STAGES = 8;  // A stages (4 KB each)
+#ifndef B2_BC_STAGES
+#define B2_BC_STAGES 8
+#endif
+constexpr int BC_STAGES = B2_BC_STAGES;  // A stages (4 KB each)
 constexpr int BC_NEPI = 8;    // epilogue warps (two per TMEM lane quarter)
-constexpr int BC_RAW = 3;     // raw byte bands in flight (TMA, two tiles ahead of the producers)
+#ifndef B2_BC_RAW
+#define B2_BC_RAW 3
+#endif
+constexpr int BC_RAW = B2_BC_RAW;  // raw byte bands in flight per group (TMA, BC_RAW - 1 tiles ahead of the producers)
 constexpr int BC_RAW_BYTES = 4096;  // per raw band: (128 / W + 2 pad) rows x W c bytes
 
 template <int BN>
@@ -266,10 +272,8 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
       tma_load_2d(graw + slot * BC_RAW_BYTES, &xmap, &grfull[slot], 0, (int)(n * g.H) + y0 - g.pad);
     };
     const int64_t t0 = blockIdx.x + (int64_t)grp * gridDim.x;
-    if (pt == 0) {
-      issue(t0, 0);
-      issue(t0 + gstep, 1);
-    }
+    if (pt == 0)
+      for (int r = 0; r + 1 < BC_RAW; ++r) issue(t0 + r * gstep, r);
     int rs = 0;
     uint32_t rph = 0;
     const uint32_t cmask = (1u << g.c) - 1u;
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(32 * (4 + BC_NPW + BC_NEPI), 1)
     int cur = 0;
     int64_t i = grp;  // index of tile t among this CTA's tiles: A stage i % BC_STAGES
     for (int64_t t = t0; t < tiles; t += gstep, cur ^= 1, i += BC_GROUPS) {
-      if (pt == 0) issue(t + 2 * gstep, rs == 0 ? 2 : rs - 1);  // the slot this group's previous tile used
+      if (pt == 0) issue(t + (BC_RAW - 1) * gstep, rs == 0 ? BC_RAW - 1 : rs - 1);  // the slot this group's previous tile used
       const uint32_t n = (uint32_t)t / g.tpi;
       const int y0 = (int)(((uint32_t)t - n * g.tpi) * BM) >> g.wshift;
       mbar_wait(&grfull[rs], rph);
